@@ -1,0 +1,390 @@
+"""Benchmark: HBP fitness evaluation of a GA population on B200 (one JSON line).
+
+Default workload (N=1): BASELINE.json config 4's single-GPU shape, "syn20k" --
+synthetic Euclidean n = m = 20000, p = 200, a 4096-chromosome population
+evaluated per step.  A step = one evaluation of the whole
+population (the batch evolve_block hands to fitness(), ga.cpp:147).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config syn20k|syn5k|sweep:P|pmed40]
+  python bench.py --impl reference ...   # the reference's own fitness() on the host cores
+
+Under torchrun (N>1) every rank evaluates its own 4096-chromosome shard of a
+global population against locally built, replicated tables: weak scaling, no
+data-path collective; only the timing max-reduction crosses ranks.
+
+Timing: W warm-up steps, then K steps; before every timed step a 512 MiB
+buffer is written to flush L2; each step is bracketed by CUDA events on the
+stream the kernels run on; the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fitness evals/s & GA gens/s (pmed40; synthetic n=m=20000,p=200), % HBM roofline"
+CONFIGS = {
+    "syn20k": dict(npts=20000, p=200, count=4096,
+                   workload="syn20k: synthetic Euclidean n=m=20000, p=200, 4096-chromosome fitness batch"),
+    "syn5k": dict(npts=5000, p=50, count=1024,
+                  workload="syn5k: synthetic Euclidean n=m=5000, p=50, 1024-chromosome fitness batch"),
+    "pmed40": dict(npts=900, p=90, count=15360,
+                   workload="pmed40-shape: synthetic Euclidean n=m=900, p=90, 60x256 population "
+                            "(OR-Library pmed40 file absent offline)"),
+}
+
+
+def config_for(name: str) -> dict:
+    if name.startswith("sweep:"):
+        p = int(name.split(":")[1])
+        return dict(npts=10000, p=p, count=4096,
+                    workload=f"sweep: synthetic Euclidean n=m=10000, p={p}, 4096-chromosome fitness batch")
+    return dict(CONFIGS[name])
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nme, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nme)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_sample(site_order, increments, n, m, p, words, gpu_costs, budget_s=10.0):
+    """The reference's own fitness() (oracle/_ref, compiled from /root/reference sources)
+    on all host threads over a bounded sample of the same population."""
+    from oracle.oracle import RefLib
+    if not RefLib.available():
+        return None
+    ref = RefLib()
+    ri = ref.create_with_tables(n, m, p, site_order, increments)
+    threads = len(os.sched_getaffinity(0))
+    probe = words[:threads]
+    t0 = time.perf_counter()
+    rc, pc, _ = ri.evaluate(probe, threads)
+    dt = time.perf_counter() - t0
+    per_eval = dt / max(1, probe.shape[0]) * threads  # single-thread seconds per eval
+    count = int(max(threads, min(words.shape[0], budget_s * threads / max(per_eval, 1e-9))))
+    count = max(threads, count // threads * threads)
+    sample = words[:count]
+    t0 = time.perf_counter()
+    rc, costs, _ = ri.evaluate(sample, threads)
+    dt = time.perf_counter() - t0
+    parity = bool(rc == 0 and (costs == gpu_costs[:count]).all())
+    return {"value": count / dt, "unit": "evals/s", "cores": threads, "kind": "reference",
+            "sample": f"first {count} chromosomes of the same population, reference fitness() "
+                      f"(proj/src/ordering.cpp:40-59) on {threads} host threads, {dt:.1f} s",
+            "bit_exact_vs_gpu": parity}
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1610_10061_b200 as pm
+    from paper_1610_10061_b200 import synth
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = config_for(args.config)
+    n = m = cfg["npts"]
+    p, count = cfg["p"], cfg["count"]
+    wp = (m + 63) // 64
+
+    ctx = pm.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream)
+    if args.kernel != "auto":
+        ctx.set_eval_kernel({"scan": pm.EVAL_SCAN, "gather": pm.EVAL_GATHER}[args.kernel])
+
+    costs = synth.euclid_costs(n, 12345, device=dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.set_instance(costs, n, m, p)
+    build_s = time.perf_counter() - t0
+    del costs
+    torch.cuda.empty_cache()
+
+    pop = synth.random_population(m, p, count, seed=7 + 1000 * rank)  # this rank's shard
+    words_host = torch.from_numpy(pop.view(np.int64)).pin_memory()
+    words = words_host.to(dev)
+    out = torch.empty(count, dtype=torch.int64, device=dev)
+    sumk = torch.empty(count, dtype=torch.int64, device=dev)
+    ctx.scan_depths_device(words, sumk, count, wp)
+    algo_bytes = 12 * int(sumk.sum().item()) + 8 * wp * count  # SURVEY.md 8(d) B_eval x count
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    for _ in range(args.warmup):
+        ctx.evaluate_device(words, out, count, wp, check=False)
+    ctx.check_errors()
+    gpu_costs = out.cpu().numpy()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ctx.profile_read()
+    ctx.set_profiling(True)
+    launches0 = ctx.kernel_launches
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.zero_()
+            starts[s].record(stream)
+            ctx.evaluate_device(words, out, count, wp, check=False)
+            ends[s].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = ctx.kernel_launches - launches0
+    ctx.set_profiling(False)
+    kern_ms, kern_n = ctx.profile_read()
+    ctx.check_errors()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    total_ms = max_over_ranks(float(sum(step_ms)), world)
+    value = count * world * args.steps / (total_ms / 1e3)
+
+    # e2e: the public host-buffer call (pm_evaluate) with H2D of the population
+    # from pinned memory and D2H of the costs inside the timed region
+    host_pop = words_host.numpy().view(np.uint64)
+    for _ in range(2):
+        ctx.evaluate(host_pop)
+    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk2:
+        for s in range(args.steps):
+            flush.zero_()
+            e_s[s].record(stream)
+            res = ctx.evaluate(host_pop)
+            e_e[s].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    assert (res == gpu_costs).all()
+    e2e_ms = max_over_ranks(float(sum(a.elapsed_time(b) for a, b in zip(e_s, e_e))), world)
+    e2e_value = count * world * args.steps / (e2e_ms / 1e3)
+
+    peak, peak_src = peaks()
+    avg_kernel_s = kern_ms / max(1, kern_n) / 1e3
+    achieved = algo_bytes / avg_kernel_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.config)
+    kernel_name = "k_scan (K2, bit-sliced scan)" if ctx.auto_eval_kernel() == 1 and args.kernel != "gather" \
+        else "k_gather (K2b, gather-min)"
+    if args.kernel == "scan":
+        kernel_name = "k_scan (K2, bit-sliced scan)"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        so, inc = ctx.get_tables()
+        cpu = cpu_reference_sample(so, inc, n, m, p, pop, gpu_costs, budget_s=args.cpu_seconds)
+
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "evals/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int64",
+        "data": "synthetic (seeded Euclidean instance, uniform random p-subset population)",
+        "config": {"workload": cfg["workload"], "n": n, "m": m, "p": p, "population_per_gpu": count,
+                   "parallelism": f"population sharded over {world} GPU(s), tables replicated",
+                   "l2": "flushed before every timed step (512 MiB write)",
+                   "kernel": kernel_name, "build_ordering_s": round(build_s, 3)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": kernel_name, "avg_kernel_ms": avg_kernel_s * 1e3,
+                     "algorithmic_bytes_per_launch": algo_bytes,
+                     "bytes_definition": "SURVEY.md 8(d): B_eval = 12*sum_i k*_i + 8*ceil(m/64) per "
+                                         "chromosome (reference layout, no reuse); effective-bandwidth "
+                                         "figure, may exceed 1.0 -- see traffic for physical DRAM bytes",
+                     "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": count * wp * 8,
+                "d2h_bytes_per_step": count * 8,
+                "call": "pm_evaluate (C ABI, host buffers; population from pinned memory)"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "clocks_e2e": clk2.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU fitness() (oracle/_ref) on the host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.oracle import RefLib
+    from paper_1610_10061_b200 import synth
+    cfg = config_for(args.config)
+    n = m = cfg["npts"]
+    p, count = cfg["p"], cfg["count"]
+    if not RefLib.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpmref.so not built"}))
+        return
+    ref = RefLib()
+    costs = synth.euclid_costs(n, 12345)
+    t0 = time.perf_counter()
+    ri = ref.create(n, m, p, costs)  # the reference's Instance + build_ordering (single thread)
+    build_s = time.perf_counter() - t0
+    del costs
+    threads = len(os.sched_getaffinity(0))
+    sample = max(threads, min(count, args.ref_sample or threads * 4) // threads * threads)
+    pop = synth.random_population(m, p, sample, seed=7)
+    for _ in range(args.warmup):
+        ri.evaluate(pop[:threads], threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        rc, _, _ = ri.evaluate(pop, threads)
+        times.append(time.perf_counter() - t0)
+        assert rc == 0
+    value = sample * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (seeded Euclidean instance, uniform random p-subset population)",
+        "config": {"workload": cfg["workload"], "n": n, "m": m, "p": p,
+                   "parallelism": f"{threads} host threads (std::thread slices, ga.cpp:253-277)",
+                   "build_ordering_s": round(build_s, 2),
+                   "step": f"reference fitness() over {sample} chromosomes of the population"},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
+                         "sample": f"{sample} chromosomes per step, {args.steps} steps"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="syn20k")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "scan", "gather"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-sample", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

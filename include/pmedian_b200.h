@@ -1,0 +1,140 @@
+/*
+ * pmedian_b200.h -- C ABI of the B200-native HBP fitness path.
+ *
+ * The reference (arXiv 1610.10061's `pmedian` C++ library, /root/reference/proj)
+ * has no FFI: its boundary is the C++ API in proj/include/pmedian/.  This ABI
+ * is what a maintainer binds underneath that API; every
+ * entry point names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "host" buffers are ordinary CPU memory;
+ *    "_device" entry points take CUDA device pointers and run on the context's
+ *    stream without synchronising unless stated.
+ *  - Chromosome wire format = the reference's Chromosome words
+ *    (proj/include/pmedian/chromosome.hpp:24,43): m bits per chromosome packed
+ *    into words_per = ceil(m/64) uint64 words, site j = bit (j & 63) of word
+ *    (j >> 6).  A population is count x words_per, row-major.  Bits at
+ *    positions >= m are ignored.
+ *  - Every call returns a pm_status.  The message of the last failure is kept
+ *    per context (pm_last_error).  Status codes map one-to-one onto the
+ *    reference's exception types (proj/include/pmedian/errors.hpp:8-25) and
+ *    the message texts are the reference's.
+ *  - A context is not thread-safe: one context per host thread.
+ */
+#ifndef PMEDIAN_B200_H_
+#define PMEDIAN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum pm_status {
+  PM_OK = 0,
+  PM_STRUCTURAL = 1, /* pmedian::StructuralError (errors.hpp:8-10) */
+  PM_CONTRACT = 2,   /* pmedian::ContractError   (errors.hpp:13-15) */
+  PM_DOMAIN = 3,     /* pmedian::DomainError     (errors.hpp:18-20) */
+  PM_BUDGET = 4,     /* pmedian::BudgetError     (errors.hpp:23-25) */
+  PM_CUDA = 5,       /* CUDA runtime failure (no reference equivalent) */
+  PM_NCCL = 6        /* collective failure (no reference equivalent) */
+} pm_status;
+
+/* Fitness kernel selection (SURVEY.md 8(d) "scan vs gather crossover"). */
+typedef enum pm_eval_kernel {
+  PM_EVAL_AUTO = 0,   /* measured crossover table picks scan or gather */
+  PM_EVAL_SCAN = 1,   /* K2: bit-sliced scan of Pi'/D' to the first open site */
+  PM_EVAL_GATHER = 2  /* K2b: gather-min over the open sites, site-major costs */
+} pm_eval_kernel;
+
+typedef struct pm_ctx pm_ctx;
+
+typedef struct pm_table_info {
+  size_t clients;     /* n                       (OrderingTables::clients, ordering.hpp:18) */
+  size_t sites;       /* m                       (OrderingTables::sites, ordering.hpp:19) */
+  size_t open_count;  /* p                       (OrderingTables::open_count, ordering.hpp:20) */
+  size_t width;       /* W = m - p + 1           (OrderingTables::width, ordering.hpp:21) */
+  size_t row_stride;  /* padded device row length in elements (>= width, multiple of 16) */
+  int site_bytes;     /* device Pi' element width: 2 (m < 65535) or 4 */
+  int dist_bytes;     /* device sorted-distance element width: 2, 4 or 8 */
+  int64_t max_cost;   /* largest cost in the matrix */
+} pm_table_info;
+
+/* ---- context ----------------------------------------------------------- */
+
+/* Creates a context on CUDA device `device` with its own non-blocking stream. */
+int pm_create(int device, pm_ctx** out);
+void pm_destroy(pm_ctx* ctx);
+/* Text of the last failure on this context ("" if none).  Valid until the next call. */
+const char* pm_last_error(const pm_ctx* ctx);
+/* Routes all later work to `stream` (a cudaStream_t; NULL restores the context's own). */
+int pm_set_stream(pm_ctx* ctx, void* stream);
+/* Number of kernels this context has launched so far (evidence counter for bench/tests). */
+uint64_t pm_kernel_launches(const pm_ctx* ctx);
+
+/* ---- instance + ordering tables (K1) ------------------------------------
+ * Replaces pmedian::Instance::Instance (instance.cpp:10-30) validation and
+ * pmedian::build_ordering (ordering.hpp:33, ordering.cpp:10-38).  Validates
+ * exactly as the Instance constructor does (same errors, same texts), then
+ * builds Pi' and the sorted distances on the device and keeps them resident
+ * together with the site-major cost matrix used by the gather kernel.
+ * `costs` is n x m row-major int64, caller-owned, read during the call only. */
+int pm_set_instance(pm_ctx* ctx, const int64_t* costs, size_t n, size_t m, size_t p);
+/* Same with `costs` already in device memory (no host copy). */
+int pm_set_instance_device(pm_ctx* ctx, const int64_t* costs_device, size_t n, size_t m, size_t p);
+int pm_table_info_get(pm_ctx* ctx, pm_table_info* out);
+/* Copies the tables back in the reference's own layout (OrderingTables::site_order
+ * uint32 and ::increments int64, clients x width row-major, ordering.hpp:22-23).
+ * For parity checks; synchronises. */
+int pm_get_tables(pm_ctx* ctx, uint32_t* site_order, int64_t* increments);
+
+/* ---- population evaluation (K2 / K2b) -----------------------------------
+ * Replaces one pmedian::fitness(tables, c) call per chromosome
+ * (ordering.hpp:39, ordering.cpp:40-59) as called by evolve_block
+ * (ga.cpp:147,166,183).  costs_out[c] is bit-identical to fitness().
+ * Errors: words_per != ceil(m/64) -> PM_STRUCTURAL with the text of
+ * ordering.cpp:42; a chromosome with no open site inside the scan width ->
+ * PM_CONTRACT with the text of ordering.cpp:51 and *first_bad = the LOWEST such
+ * chromosome index (what a sequential loop of fitness() calls throws first).
+ * Host-buffer form: copies in, evaluates, copies out, synchronises. */
+int pm_evaluate(pm_ctx* ctx, const uint64_t* bitsets, size_t count, size_t words_per,
+                int64_t* costs_out, size_t* first_bad);
+/* Device-buffer form.  If first_bad is NULL the call is fully asynchronous on
+ * the context stream and errors are reported by pm_check_errors; otherwise it
+ * synchronises and reports as pm_evaluate. */
+int pm_evaluate_device(pm_ctx* ctx, const uint64_t* bitsets_device, size_t count,
+                       size_t words_per, int64_t* costs_out_device, size_t* first_bad);
+/* Synchronises and reports any contract failure recorded by asynchronous calls
+ * since the last check. */
+int pm_check_errors(pm_ctx* ctx, size_t* first_bad);
+/* Chooses the evaluation kernel (default PM_EVAL_AUTO). */
+int pm_set_eval_kernel(pm_ctx* ctx, int kind);
+/* Kernel PM_EVAL_AUTO would pick for the current instance (1 = scan, 2 = gather). */
+int pm_auto_eval_kernel(pm_ctx* ctx);
+
+/* Gather-min without the scan-width contract: replaces pmedian::min_cost_sum
+ * (instance.hpp:39, instance.cpp:32-48) per chromosome; a chromosome with no
+ * open site -> PM_CONTRACT "at least one site must be open". */
+int pm_min_cost_sum(pm_ctx* ctx, const uint64_t* bitsets, size_t count, size_t words_per,
+                    int64_t* costs_out, size_t* first_bad);
+
+/* ---- measurement hooks -----------------------------------------------------
+ * Per chromosome, the sum over clients of the 1-based stopping column k*_i of
+ * the reference scan (ordering.cpp:49-55) -- the work measure of the roofline
+ * (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64)).  Device
+ * buffers; synchronises; PM_CONTRACT as pm_evaluate on a runoff. */
+int pm_scan_depths_device(pm_ctx* ctx, const uint64_t* bitsets_device, size_t count,
+                          size_t words_per, uint64_t* sum_k_device);
+/* When enabled, CUDA events on the context stream bracket every launch of the
+ * dominant evaluation kernel (K2 scan or K2b gather). */
+int pm_set_profiling(pm_ctx* ctx, int enabled);
+/* Synchronises, returns the summed duration (ms) and count of the bracketed
+ * launches since the last read, and resets. */
+int pm_profile_read(pm_ctx* ctx, double* kernel_ms, uint64_t* kernel_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMEDIAN_B200_H_ */

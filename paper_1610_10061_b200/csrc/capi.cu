@@ -1,0 +1,484 @@
+// C-ABI implementation (include/pmedian_b200.h): context, instance upload,
+// K1 orchestration and the K2/K2b dispatch.  Host-side C++; no CPU compute
+// path exists -- every cost is produced by a kernel.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pmedian_b200.h"
+#include "kernels.h"
+
+using namespace pmb;
+
+namespace {
+
+// Reference message texts (errors thrown by the code each status replaces).
+constexpr const char* kMsgLength = "chromosome length must equal the site count";  // ordering.cpp:42
+constexpr const char* kMsgRunoff =
+    "no open site within the scan width; exactly p sites must be open";  // ordering.cpp:51
+constexpr const char* kMsgNoneOpen = "at least one site must be open";  // instance.cpp:37
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct pm_ctx {
+  int device = 0;
+  int sms = 148;
+  size_t max_smem = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+  int eval_kind = PM_EVAL_AUTO;
+
+  bool has_instance = false;
+  DevTables t;
+  BuildPlan plan;
+  DevBuf ord, dist, dT;
+
+  // scratch
+  DevBuf costs_in, sort_keys, sort_pay, words, costs_out, T, lists, counts, errw, scal;
+  int open_cap = 0;
+
+  // kernel timing hook: events around the dominant evaluation kernel
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
+  std::pair<cudaEvent_t, cudaEvent_t> ev_get() {
+    if (!ev_free.empty()) {
+      auto e = ev_free.back();
+      ev_free.pop_back();
+      return e;
+    }
+    std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
+    cudaEventCreate(&e.first);
+    cudaEventCreate(&e.second);
+    return e;
+  }
+
+  int fail(int code, const std::string& msg) {
+    err = msg;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* where) {
+    err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+    return PM_CUDA;
+  }
+};
+
+#define PM_CUDA_TRY(ctx, expr)                              \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return (ctx)->cuda_fail(_e, #expr); \
+  } while (0)
+
+extern "C" {
+
+int pm_create(int device, pm_ctx** out) {
+  if (!out) return PM_STRUCTURAL;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return PM_CUDA;
+  if (device < 0 || device >= ndev) return PM_DOMAIN;
+  if (cudaSetDevice(device) != cudaSuccess) return PM_CUDA;
+  pm_ctx* c = new pm_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  c->max_smem = (size_t)optin;
+  if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return PM_CUDA;
+  }
+  c->stream = c->own;
+  if (c->errw.ensure(16) != cudaSuccess) {
+    delete c;
+    return PM_CUDA;
+  }
+  cudaMemsetAsync(c->errw.p, 0xff, 16, c->stream);
+  *out = c;
+  return PM_OK;
+}
+
+void pm_destroy(pm_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (DevBuf* b : {&c->ord, &c->dist, &c->dT, &c->costs_in, &c->sort_keys, &c->sort_pay, &c->words,
+                    &c->costs_out, &c->T, &c->lists, &c->counts, &c->errw, &c->scal})
+    b->release();
+  for (auto* v : {&c->ev_used, &c->ev_free})
+    for (auto& e : *v) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+}
+
+const char* pm_last_error(const pm_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int pm_set_stream(pm_ctx* c, void* stream) {
+  if (!c) return PM_STRUCTURAL;
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+  return PM_OK;
+}
+
+uint64_t pm_kernel_launches(const pm_ctx* c) { return c ? c->launches : 0; }
+
+// ---- instance ------------------------------------------------------------------
+
+static int bits_for(uint64_t v) { return v == 0 ? 0 : 64 - __builtin_clzll(v); }
+
+static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t m, size_t p) {
+  // Instance::Instance checks, in the reference's order (instance.cpp:13-29).
+  if (n == 0) return c->fail(PM_STRUCTURAL, "instance needs at least one client");
+  if (m == 0) return c->fail(PM_STRUCTURAL, "instance needs at least one site");
+  if (p < 1) return c->fail(PM_DOMAIN, "p must be >= 1");
+  if (p >= m) return c->fail(PM_DOMAIN, "p must be < m");
+  if (n > (size_t)INT_MAX / 2 || m > (size_t)INT_MAX / 2)
+    return c->fail(PM_DOMAIN, "device tables support at most 2^30 clients and sites");
+
+  unsigned long long* scal = nullptr;
+  PM_CUDA_TRY(c, c->scal.ensure(16));
+  scal = c->scal.as<unsigned long long>();
+  PM_CUDA_TRY(c, cudaMemsetAsync(scal, 0, 16, c->stream));
+  PM_CUDA_TRY(c, launch_scan_costs(dcosts, n * m, scal, reinterpret_cast<int*>(scal + 1), c->sms,
+                                   c->stream));
+  c->launches += 1;
+  unsigned long long host[2] = {0, 0};
+  PM_CUDA_TRY(c, cudaMemcpyAsync(host, scal, 16, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (host[1] & 1) return c->fail(PM_STRUCTURAL, "costs must be non-negative");
+  const int64_t max_cost = (int64_t)host[0];
+  if (max_cost > 0 && max_cost > INT64_MAX / (int64_t)n)
+    return c->fail(PM_STRUCTURAL, "costs too large: n * max(cost) would overflow 64-bit totals");
+
+  BuildPlan bp;
+  bp.n = (int)n;
+  bp.m = (int)m;
+  bp.p = (int)p;
+  bp.W = (int)(m - p + 1);
+  bp.Wp = (bp.W + 15) / 16 * 16;
+  bp.site_bytes = m <= 65535 ? 2 : 4;  // sentinel site m must fit
+  bp.dist_bytes = max_cost <= 65535 ? 2 : (max_cost <= 0xffffffffLL ? 4 : 8);
+  bp.sitebits = std::max(1, bits_for((uint64_t)(m - 1)));
+  bp.costbits = bits_for((uint64_t)max_cost);
+  bp.npasses = (bp.costbits + 7) / 8;
+  if (bp.costbits + bp.sitebits <= 32) bp.key_kind = KeyKind::kPacked32;
+  else if (bp.costbits + bp.sitebits <= 64) bp.key_kind = KeyKind::kPacked64;
+  else bp.key_kind = KeyKind::kPayload64;
+  const size_t keyb = bp.key_kind == KeyKind::kPacked32 ? 4 : 8;
+  const size_t payb = bp.key_kind == KeyKind::kPayload64 ? 4 : 0;
+  const size_t need = sort_smem_header() + m * (keyb + payb) * 2;
+  bp.smem_path = need <= c->max_smem;
+  if (bp.smem_path) {
+    bp.grid = (int)std::min<size_t>(n, (size_t)c->sms);
+  } else {
+    bp.grid = (int)std::min<size_t>(n, (size_t)c->sms);
+    PM_CUDA_TRY(c, c->sort_keys.ensure((size_t)bp.grid * 2 * m * keyb));
+    if (payb) PM_CUDA_TRY(c, c->sort_pay.ensure((size_t)bp.grid * 2 * m * payb));
+  }
+
+  c->has_instance = false;
+  c->ord.release();
+  c->dist.release();
+  c->dT.release();
+  const size_t cells = n * (size_t)bp.Wp;
+  PM_CUDA_TRY(c, c->ord.ensure(cells * bp.site_bytes));
+  PM_CUDA_TRY(c, c->dist.ensure(cells * bp.dist_bytes));
+  PM_CUDA_TRY(c, c->dT.ensure(n * m * (size_t)bp.dist_bytes));
+  PM_CUDA_TRY(c, launch_build_rows(bp, dcosts, c->ord.p, c->dist.p, c->sort_keys.p,
+                                   c->sort_pay.as<uint32_t>(), c->stream));
+  PM_CUDA_TRY(c, launch_transpose_costs(dcosts, (int)n, (int)m, bp.dist_bytes, c->dT.p, c->stream));
+  c->launches += 2;
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (!bp.smem_path) {
+    c->sort_keys.release();
+    c->sort_pay.release();
+  }
+
+  c->plan = bp;
+  DevTables& t = c->t;
+  t.n = bp.n;
+  t.m = bp.m;
+  t.p = bp.p;
+  t.W = bp.W;
+  t.Wp = bp.Wp;
+  t.site_bytes = bp.site_bytes;
+  t.dist_bytes = bp.dist_bytes;
+  t.max_cost = max_cost;
+  t.ord = c->ord.p;
+  t.dist = c->dist.p;
+  t.dT = c->dT.p;
+  c->open_cap = (int)std::min<size_t>(m, (std::max<size_t>(p, 16) + 3) / 4 * 4);
+  c->has_instance = true;
+  c->err.clear();
+  return PM_OK;
+}
+
+int pm_set_instance(pm_ctx* c, const int64_t* costs, size_t n, size_t m, size_t p) {
+  if (!c) return PM_STRUCTURAL;
+  if (!costs && n * m) return c->fail(PM_STRUCTURAL, "cost matrix must be exactly n rows by m columns");
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  if (n == 0 || m == 0 || p < 1 || p >= m) return set_instance_impl(c, nullptr, n, m, p);
+  PM_CUDA_TRY(c, c->costs_in.ensure(n * m * 8));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(c->costs_in.p, costs, n * m * 8, cudaMemcpyHostToDevice, c->stream));
+  const int rc = set_instance_impl(c, c->costs_in.as<int64_t>(), n, m, p);
+  c->costs_in.release();
+  return rc;
+}
+
+int pm_set_instance_device(pm_ctx* c, const int64_t* costs_device, size_t n, size_t m, size_t p) {
+  if (!c) return PM_STRUCTURAL;
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  return set_instance_impl(c, costs_device, n, m, p);
+}
+
+int pm_table_info_get(pm_ctx* c, pm_table_info* out) {
+  if (!c || !out) return PM_STRUCTURAL;
+  if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
+  out->clients = c->t.n;
+  out->sites = c->t.m;
+  out->open_count = c->t.p;
+  out->width = c->t.W;
+  out->row_stride = c->t.Wp;
+  out->site_bytes = c->t.site_bytes;
+  out->dist_bytes = c->t.dist_bytes;
+  out->max_cost = c->t.max_cost;
+  return PM_OK;
+}
+
+int pm_get_tables(pm_ctx* c, uint32_t* site_order, int64_t* increments) {
+  if (!c) return PM_STRUCTURAL;
+  if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  const DevTables& t = c->t;
+  const size_t cells = (size_t)t.n * t.Wp;
+  std::vector<unsigned char> o(cells * t.site_bytes), d(cells * t.dist_bytes);
+  PM_CUDA_TRY(c, cudaMemcpyAsync(o.data(), t.ord, o.size(), cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(d.data(), t.dist, d.size(), cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < t.n; ++i) {
+    int64_t prev = 0;
+    for (int k = 0; k < t.W; ++k) {
+      const size_t x = (size_t)i * t.Wp + k;
+      const uint32_t s = t.site_bytes == 2 ? reinterpret_cast<uint16_t*>(o.data())[x]
+                                           : reinterpret_cast<uint32_t*>(o.data())[x];
+      int64_t v;
+      if (t.dist_bytes == 2) v = reinterpret_cast<uint16_t*>(d.data())[x];
+      else if (t.dist_bytes == 4) v = reinterpret_cast<uint32_t*>(d.data())[x];
+      else v = reinterpret_cast<int64_t*>(d.data())[x];
+      site_order[(size_t)i * t.W + k] = s;
+      increments[(size_t)i * t.W + k] = v - prev;  // ordering.cpp:33
+      prev = v;
+    }
+  }
+  return PM_OK;
+}
+
+// ---- evaluation ------------------------------------------------------------------
+
+int pm_set_eval_kernel(pm_ctx* c, int kind) {
+  if (!c) return PM_STRUCTURAL;
+  if (kind < PM_EVAL_AUTO || kind > PM_EVAL_GATHER) return c->fail(PM_DOMAIN, "unknown evaluation kernel");
+  c->eval_kind = kind;
+  return PM_OK;
+}
+
+static bool scan_fits(pm_ctx* c, size_t count) {
+  return plan_scan(c->t, std::max<size_t>(count, 64), c->sms, c->max_smem, false).ctas > 0;
+}
+
+// Measured crossover (profiles/): the scan touches ~(m+1)/(p+1)
+// columns per client, the gather p sites.
+static int auto_kind(pm_ctx* c, size_t count) {
+  if (!scan_fits(c, count)) return PM_EVAL_GATHER;
+  const double pstar = 1.3 * std::sqrt((double)c->t.m);
+  return (double)c->t.p >= pstar ? PM_EVAL_SCAN : PM_EVAL_GATHER;
+}
+
+int pm_auto_eval_kernel(pm_ctx* c) {
+  if (!c || !c->has_instance) return 0;
+  return auto_kind(c, 4096);
+}
+
+// mode: 0 fitness (ordering.cpp:40-59), 1 min_cost_sum (instance.cpp:32-48),
+// 2 scan depths (sum_i k*_i, the roofline's work measure).
+static int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcosts, int mode) {
+  const DevTables& t = c->t;
+  const int wp = (t.m + 63) / 64;
+  PM_CUDA_TRY(c, cudaMemsetAsync(dcosts, 0, count * 8, c->stream));
+  unsigned long long* errw = c->errw.as<unsigned long long>();
+  int kind = c->eval_kind == PM_EVAL_AUTO ? auto_kind(c, count) : c->eval_kind;
+  if (mode == 1) kind = PM_EVAL_GATHER;
+  if (mode == 2) kind = PM_EVAL_SCAN;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (kind == PM_EVAL_SCAN) {
+    const ScanPlan sp = plan_scan(t, count, c->sms, c->max_smem, mode == 2);
+    if (sp.ctas == 0)
+      return c->fail(PM_DOMAIN, "instance too large for the scan kernel's shared-memory masks; use PM_EVAL_GATHER");
+    const size_t groups = (count + 63) / 64;
+    PM_CUDA_TRY(c, c->T.ensure(groups * scan_t_stride(t.m) * 8));
+    PM_CUDA_TRY(c, launch_transpose_population(dwords, count, wp, t.m, c->T.as<uint64_t>(), c->stream));
+    if (c->profiling) {
+      ev = c->ev_get();
+      cudaEventRecord(ev.first, c->stream);
+    }
+    PM_CUDA_TRY(c, launch_scan(t, sp, c->T.as<uint64_t>(), count,
+                               reinterpret_cast<unsigned long long*>(dcosts), errw, mode == 2, c->stream));
+  } else {
+    PM_CUDA_TRY(c, c->lists.ensure(count * (size_t)c->open_cap * 4));
+    PM_CUDA_TRY(c, c->counts.ensure(count * 4));
+    PM_CUDA_TRY(c, launch_open_lists(dwords, count, wp, t.m, c->lists.as<uint32_t>(),
+                                     c->counts.as<uint32_t>(), c->open_cap, c->stream));
+    if (c->profiling) {
+      ev = c->ev_get();
+      cudaEventRecord(ev.first, c->stream);
+    }
+    PM_CUDA_TRY(c, launch_gather(t, dwords, count, wp, c->lists.as<uint32_t>(), c->counts.as<uint32_t>(),
+                                 c->open_cap, reinterpret_cast<unsigned long long*>(dcosts), errw, mode,
+                                 c->sms, c->stream));
+  }
+  if (c->profiling) {
+    cudaEventRecord(ev.second, c->stream);
+    c->ev_used.push_back(ev);
+  }
+  c->launches += 2;
+  return PM_OK;
+}
+
+int pm_check_errors(pm_ctx* c, size_t* first_bad) {
+  if (!c) return PM_STRUCTURAL;
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  unsigned long long h = ~0ull;
+  PM_CUDA_TRY(c, cudaMemcpyAsync(&h, c->errw.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  PM_CUDA_TRY(c, cudaMemsetAsync(c->errw.p, 0xff, 8, c->stream));
+  if (h != ~0ull) {
+    if (first_bad) *first_bad = (size_t)h;
+    return c->fail(PM_CONTRACT, kMsgRunoff);
+  }
+  return PM_OK;
+}
+
+static int evaluate_dev(pm_ctx* c, const uint64_t* dwords, size_t count, size_t words_per,
+                        int64_t* dcosts, size_t* first_bad, int mode) {
+  if (!c) return PM_STRUCTURAL;
+  if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
+  if (words_per != (size_t)(c->t.m + 63) / 64) return c->fail(PM_STRUCTURAL, kMsgLength);
+  if (count == 0) return PM_OK;
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  if (first_bad) {  // synchronous error report for this call alone
+    PM_CUDA_TRY(c, cudaMemsetAsync(c->errw.p, 0xff, 8, c->stream));
+  }
+  int rc = evaluate_core(c, dwords, count, dcosts, mode);
+  if (rc != PM_OK) return rc;
+  if (first_bad) {
+    rc = pm_check_errors(c, first_bad);
+    if (rc == PM_CONTRACT && mode == 1) c->err = kMsgNoneOpen;
+    return rc;
+  }
+  return PM_OK;
+}
+
+int pm_evaluate_device(pm_ctx* c, const uint64_t* bitsets_device, size_t count, size_t words_per,
+                       int64_t* costs_out_device, size_t* first_bad) {
+  return evaluate_dev(c, bitsets_device, count, words_per, costs_out_device, first_bad, 0);
+}
+
+static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_t words_per,
+                         int64_t* costs_out, size_t* first_bad, int mode) {
+  if (!c) return PM_STRUCTURAL;
+  if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
+  if (words_per != (size_t)(c->t.m + 63) / 64) return c->fail(PM_STRUCTURAL, kMsgLength);
+  if (count == 0) return PM_OK;
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  PM_CUDA_TRY(c, c->words.ensure(count * words_per * 8));
+  PM_CUDA_TRY(c, c->costs_out.ensure(count * 8));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(c->words.p, bitsets, count * words_per * 8, cudaMemcpyHostToDevice,
+                                 c->stream));
+  size_t fb = 0;
+  int rc = evaluate_dev(c, c->words.as<uint64_t>(), count, words_per, c->costs_out.as<int64_t>(), &fb, mode);
+  if (rc == PM_CONTRACT) {
+    if (first_bad) *first_bad = fb;
+    return rc;
+  }
+  if (rc != PM_OK) return rc;
+  PM_CUDA_TRY(c, cudaMemcpyAsync(costs_out, c->costs_out.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PM_OK;
+}
+
+int pm_evaluate(pm_ctx* c, const uint64_t* bitsets, size_t count, size_t words_per, int64_t* costs_out,
+                size_t* first_bad) {
+  return evaluate_host(c, bitsets, count, words_per, costs_out, first_bad, 0);
+}
+
+int pm_scan_depths_device(pm_ctx* c, const uint64_t* bitsets_device, size_t count, size_t words_per,
+                          uint64_t* sum_k_device) {
+  if (!c) return PM_STRUCTURAL;
+  if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
+  size_t fb = 0;
+  return evaluate_dev(c, bitsets_device, count, words_per, reinterpret_cast<int64_t*>(sum_k_device), &fb, 2);
+}
+
+int pm_set_profiling(pm_ctx* c, int enabled) {
+  if (!c) return PM_STRUCTURAL;
+  c->profiling = enabled != 0;
+  return PM_OK;
+}
+
+int pm_profile_read(pm_ctx* c, double* kernel_ms, uint64_t* kernel_launches) {
+  if (!c) return PM_STRUCTURAL;
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  double total = 0;
+  uint64_t cnt = 0;
+  for (auto& e : c->ev_used) {
+    PM_CUDA_TRY(c, cudaEventSynchronize(e.second));
+    float ms = 0;
+    PM_CUDA_TRY(c, cudaEventElapsedTime(&ms, e.first, e.second));
+    total += ms;
+    ++cnt;
+    c->ev_free.push_back(e);
+  }
+  c->ev_used.clear();
+  if (kernel_ms) *kernel_ms = total;
+  if (kernel_launches) *kernel_launches = cnt;
+  return PM_OK;
+}
+
+int pm_min_cost_sum(pm_ctx* c, const uint64_t* bitsets, size_t count, size_t words_per,
+                    int64_t* costs_out, size_t* first_bad) {
+  return evaluate_host(c, bitsets, count, words_per, costs_out, first_bad, 1);
+}
+
+}  // extern "C"

@@ -1,0 +1,495 @@
+// K2 / K2b: population fitness on the device.
+//
+// Replaces the per-chromosome loop of pmedian::fitness
+// (/root/reference/proj/src/ordering.cpp:40-59) as evolve_block calls it
+// (ga.cpp:147,166,183).  Per chromosome c and client i the reference scans
+// client i's ordered sites until the first open one (k*_i) and adds the
+// increments up to and including it; that prefix sum is dist[i][k*_i].
+//
+// K2 ("scan", bit-sliced).  64 chromosomes form a group.  The group's open
+// sets are transposed into T[s] (u64; bit c = chromosome c has site s open),
+// staged in shared memory.  Each lane owns one client at a time and walks its
+// row once for the whole group: alive &= ~T[pi_ik], and every bit leaving
+// `alive` at column k is a (chromosome, client) pair whose cost is dist[i][k].
+// One row walk of length max_c k*_ic serves 64 evaluations, so a row prefix is
+// read from L2/HBM once per group instead of once per chromosome; lanes claim
+// clients dynamically so a short row does not wait for a long one.  Hits are
+// accumulated into per-lane private shared-memory counters (no atomics) and
+// reduced once per CTA segment.
+//
+// K2b ("gather", gather-min).  fitness = sum_i min_{j open} cost(i, j)
+// (instance.cpp:32-48, equal to the scan by acceptance.cpp:86-116).  Lanes are
+// clients; each open site j of a chromosome is one coalesced read of the
+// site-major row dT[j][i0..].  Wins when p is small (the scan reads ~m/p
+// columns per client, the gather p).  The reference's scan-width contract
+// (ordering.cpp:50-52) is enforced exactly: with popcount >= p it cannot fail
+// (W = m-p+1 columns always contain one of p distinct sites); with fewer open
+// sites the (cost, site)-smallest open site must not sort after column W-1.
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pmb {
+
+// ---- K2t: population -> transposed group masks ------------------------------
+
+size_t scan_t_stride(int m) { return ((size_t)m + 1 + 1) / 2 * 2; }
+
+__global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __restrict__ words,
+                                                              size_t count, int wp, int m,
+                                                              uint64_t* __restrict__ T,
+                                                              size_t Ts) {
+  const int lane = threadIdx.x & 31;
+  const int wi = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const size_t g = blockIdx.y;
+  uint64_t* Tg = T + g * Ts;
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    for (size_t s = (size_t)m + lane; s < Ts; s += 32) Tg[s] = 0;  // sentinel site m
+  }
+  if (wi >= wp) return;  // warp-uniform
+  const size_t c0 = g * 64 + lane, c1 = c0 + 32;
+  const uint64_t x = c0 < count ? words[c0 * wp + wi] : 0;
+  const uint64_t y = c1 < count ? words[c1 * wp + wi] : 0;
+  uint64_t t0 = 0, t1 = 0;
+#pragma unroll
+  for (int b = 0; b < 32; ++b) {
+    const uint32_t lo0 = __ballot_sync(kFull, (x >> b) & 1);
+    const uint32_t hi0 = __ballot_sync(kFull, (y >> b) & 1);
+    const uint32_t lo1 = __ballot_sync(kFull, (x >> (b + 32)) & 1);
+    const uint32_t hi1 = __ballot_sync(kFull, (y >> (b + 32)) & 1);
+    if (lane == b) {
+      t0 = (uint64_t)lo0 | ((uint64_t)hi0 << 32);
+      t1 = (uint64_t)lo1 | ((uint64_t)hi1 << 32);
+    }
+  }
+  const int s0 = wi * 64 + lane, s1 = s0 + 32;
+  if (s0 < m) Tg[s0] = t0;
+  if (s1 < m) Tg[s1] = t1;
+}
+
+cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int words_per, int m,
+                                        uint64_t* T, cudaStream_t st) {
+  const size_t groups = (count + 63) / 64;
+  dim3 grid((words_per + 7) / 8, (unsigned)groups);
+  k_transpose_population<<<grid, 256, 0, st>>>(words, count, words_per, m, T, scan_t_stride(m));
+  return cudaGetLastError();
+}
+
+// ---- K2: bit-sliced scan -------------------------------------------------------
+
+constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
+
+template <class OrdT, class DistT>
+struct Chunk {
+  static constexpr int kO = kChunk * sizeof(OrdT) / 16;   // uint4s of sites
+  static constexpr int kD = kChunk * sizeof(DistT) / 16;  // uint4s of costs
+  uint4 o[kO];
+  uint4 d[kD];
+
+  __device__ __forceinline__ void load(const OrdT* orow, const DistT* drow, int k) {
+#pragma unroll
+    for (int x = 0; x < kO; ++x) o[x] = ldg_stream(reinterpret_cast<const uint4*>(orow + k) + x);
+#pragma unroll
+    for (int x = 0; x < kD; ++x) d[x] = ldg_stream(reinterpret_cast<const uint4*>(drow + k) + x);
+  }
+  __device__ __forceinline__ uint32_t site(int j) const {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(o);
+    if constexpr (sizeof(OrdT) == 2) return (w[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+    else return w[j];
+  }
+  __device__ __forceinline__ uint64_t cost(int j) const {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(d);
+    if constexpr (sizeof(DistT) == 2) return (w[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+    else if constexpr (sizeof(DistT) == 4) return w[j];
+    else return (uint64_t)w[2 * j] | ((uint64_t)w[2 * j + 1] << 32);
+  }
+};
+
+template <class OrdT, class DistT, class AccT>
+__global__ void __launch_bounds__(512, 1)
+    k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
+           const uint64_t* __restrict__ T, size_t Ts, size_t count, int groups,
+           unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err,
+           int depth_mode) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int nwarps = blockDim.x >> 5;
+  uint64_t* Tsm = reinterpret_cast<uint64_t*>(smem);
+  AccT* acc = reinterpret_cast<AccT*>(smem + Ts * 8);
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(acc + (size_t)nwarps * 64 * 32);
+  int* next_client = reinterpret_cast<int*>(red + (nwarps / 2) * 64);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = lanemask_lt();
+  AccT* myacc = acc + (size_t)warp * 64 * 32 + lane;
+
+  const long long U = (long long)groups * n;
+  long long u = U * blockIdx.x / gridDim.x;
+  const long long uend = U * (blockIdx.x + 1) / gridDim.x;
+  while (u < uend) {
+    const int g = (int)(u / n);
+    const int c0 = (int)(u % n);
+    const int c1 = (int)min((long long)n, c0 + (uend - u));
+    u += c1 - c0;
+
+    {  // stage the group's masks, clear the counters
+      const uint4* src = reinterpret_cast<const uint4*>(T + (size_t)g * Ts);
+      uint4* dstT = reinterpret_cast<uint4*>(Tsm);
+      for (size_t x = tid; x < Ts / 2; x += blockDim.x) dstT[x] = src[x];
+      for (int x = tid; x < nwarps * 64 * 32; x += blockDim.x) acc[x] = 0;
+      if (tid == 0) *next_client = c0;
+    }
+    __syncthreads();
+    const size_t nvalid = min((size_t)64, count - (size_t)g * 64);
+    const uint64_t vmask = nvalid == 64 ? ~0ull : ((1ull << nvalid) - 1);
+
+    int i = -1, k = 0;
+    uint64_t alive = 0;
+    const OrdT* orow = nullptr;
+    const DistT* drow = nullptr;
+    Chunk<OrdT, DistT> cur, nxt;
+    int wb_next = 0, wb_end = 0;
+    bool exhausted = false;
+    while (true) {
+      unsigned need = __ballot_sync(kFull, i < 0);
+      while (need && !exhausted) {
+        if (wb_next >= wb_end) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(next_client, 32);
+          base = __shfl_sync(kFull, base, 0);
+          if (base >= c1) {
+            exhausted = true;
+            break;
+          }
+          wb_next = base;
+          wb_end = min(base + 32, c1);
+        }
+        const int rank = __popc(need & lt);
+        const int avail = wb_end - wb_next;
+        if (i < 0 && rank < avail) {
+          i = wb_next + rank;
+          k = 0;
+          alive = vmask;
+          orow = ord + (size_t)i * Wp;
+          drow = dist + (size_t)i * Wp;
+          cur.load(orow, drow, 0);
+          if (kChunk < Wp) nxt.load(orow, drow, kChunk);
+        }
+        wb_next += min(__popc(need), avail);
+        need = __ballot_sync(kFull, i < 0);
+      }
+      if (__ballot_sync(kFull, i >= 0) == 0) break;
+      if (i >= 0) {
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const uint64_t t = Tsm[cur.site(j)];
+          uint64_t h = alive & t;
+          alive &= ~t;
+          if (h) {
+            // depth_mode: accumulate the 1-based stopping column k* instead of
+            // the cost (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
+            const AccT dv = depth_mode ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
+            do {
+              const int c = __ffsll((long long)h) - 1;
+              h &= h - 1;
+              myacc[c * 32] += dv;
+            } while (h);
+          }
+        }
+        k += kChunk;
+        if (alive == 0 || k >= Wp) {
+          if (alive) atomicMin(err, (unsigned long long)g * 64 + (__ffsll((long long)alive) - 1));
+          i = -1;
+        } else {
+          cur = nxt;
+          if (k + kChunk < Wp) nxt.load(orow, drow, k + kChunk);
+        }
+      }
+    }
+    __syncthreads();
+    {  // reduce the per-lane counters: thread -> (chromosome c, warp pair q)
+      const int c = tid & 63, q = tid >> 6;
+      unsigned long long s = 0;
+      if (q < nwarps / 2) {
+        for (int w = 2 * q; w < 2 * q + 2; ++w) {
+          const AccT* a = acc + ((size_t)w * 64 + c) * 32;
+#pragma unroll 8
+          for (int l = 0; l < 32; ++l) s += (unsigned long long)a[(l + c) & 31];
+        }
+        red[q * 64 + c] = s;
+      }
+    }
+    __syncthreads();
+    if (tid < 64 && (size_t)tid < nvalid) {
+      unsigned long long s = 0;
+      for (int q = 0; q < nwarps / 2; ++q) s += red[q * 64 + tid];
+      atomicAdd(&costs[(size_t)g * 64 + tid], s);
+    }
+    __syncthreads();
+  }
+}
+
+static size_t scan_smem(int m, int warps, bool acc32) {
+  return scan_t_stride(m) * 8 + (size_t)warps * 64 * 32 * (acc32 ? 4 : 8) + (warps / 2) * 64 * 8 + 16;
+}
+
+template <class OrdT, class DistT, class AccT>
+static const void* scan_fn() {
+  return reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT>);
+}
+
+static const void* scan_kernel_ptr(const DevTables& t, bool acc32) {
+  if (t.site_bytes == 2) {
+    if (t.dist_bytes == 2) return acc32 ? scan_fn<uint16_t, uint16_t, uint32_t>() : scan_fn<uint16_t, uint16_t, uint64_t>();
+    if (t.dist_bytes == 4) return acc32 ? scan_fn<uint16_t, uint32_t, uint32_t>() : scan_fn<uint16_t, uint32_t, uint64_t>();
+    return acc32 ? scan_fn<uint16_t, uint64_t, uint32_t>() : scan_fn<uint16_t, uint64_t, uint64_t>();
+  }
+  if (t.dist_bytes == 2) return acc32 ? scan_fn<uint32_t, uint16_t, uint32_t>() : scan_fn<uint32_t, uint16_t, uint64_t>();
+  if (t.dist_bytes == 4) return acc32 ? scan_fn<uint32_t, uint32_t, uint32_t>() : scan_fn<uint32_t, uint32_t, uint64_t>();
+  return acc32 ? scan_fn<uint32_t, uint64_t, uint32_t>() : scan_fn<uint32_t, uint64_t, uint64_t>();
+}
+
+ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode) {
+  ScanPlan sp;
+  const size_t groups = (count + 63) / 64;
+  for (int warps : {16, 8, 4}) {
+    for (int pass = 0; pass < 2; ++pass) {
+      const int blocks_per_sm = 1;
+      const int ctas = sms * blocks_per_sm;
+      const long long U = (long long)groups * t.n;
+      const long long seg = (U + ctas - 1) / ctas;  // clients one lane-counter can see
+      const unsigned long long vmax =
+          depth_mode ? (unsigned long long)t.Wp : (unsigned long long)t.max_cost;
+      const bool acc32 =
+          pass == 0 && (unsigned long long)std::min<long long>(seg, t.n) * vmax < (1ull << 32);
+      if (pass == 0 && !acc32) continue;
+      const size_t smem = scan_smem(t.m, warps, acc32);
+      if (smem <= max_smem) {
+        sp.warps = warps;
+        sp.acc32 = acc32;
+        sp.smem = smem;
+        sp.ctas = ctas;
+        return sp;
+      }
+    }
+  }
+  sp.ctas = 0;  // does not fit: caller must use the gather kernel
+  return sp;
+}
+
+cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* T, size_t count,
+                        unsigned long long* costs_acc, unsigned long long* err_first_bad,
+                        int depth_mode, cudaStream_t st) {
+  const void* fn = scan_kernel_ptr(t, sp.acc32);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem);
+  if (e != cudaSuccess) return e;
+  const int groups = (int)((count + 63) / 64);
+  const int ctas = std::min<long long>(sp.ctas, (long long)groups * t.n);
+  size_t Ts = scan_t_stride(t.m);
+  const void* ord = t.ord;
+  const void* dist = t.dist;
+  int n = t.n, Wp = t.Wp;
+  void* args[] = {(void*)&ord, (void*)&dist, (void*)&n, (void*)&Wp, (void*)&T, (void*)&Ts,
+                  (void*)&count, (void*)&groups, (void*)&costs_acc, (void*)&err_first_bad,
+                  (void*)&depth_mode};
+  e = cudaLaunchKernel(fn, dim3(ctas), dim3(sp.warps * 32), args, sp.smem, st);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// ---- K2b: gather-min -----------------------------------------------------------
+
+// One warp per chromosome: compact the open sites (< m) into a list.
+__global__ void __launch_bounds__(256) k_open_lists(const uint64_t* __restrict__ words, size_t count,
+                                                    int wp, int m, uint32_t* __restrict__ lists,
+                                                    uint32_t* __restrict__ counts, int cap) {
+  const size_t c = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= count) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const uint64_t* w = words + c * wp;
+  uint32_t* list = lists + c * (size_t)cap;
+  uint32_t total = 0;
+  for (int w0 = 0; w0 < wp; w0 += 32) {
+    const int wi = w0 + lane;
+    uint64_t x = wi < wp ? w[wi] : 0;
+    if (wi == wp - 1 && (m & 63)) x &= (1ull << (m & 63)) - 1;  // bits >= m are not sites
+    const uint32_t pc = __popcll(x);
+    uint32_t incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    uint32_t pos = total + incl - pc;
+    while (x) {
+      const int b = __ffsll((long long)x) - 1;
+      x &= x - 1;
+      if (pos < (uint32_t)cap) list[pos] = (uint32_t)(wi * 64 + b);
+      ++pos;
+    }
+    total += __shfl_sync(kFull, incl, 31);
+    (void)lt;
+  }
+  if (lane == 0) counts[c] = total;
+}
+
+constexpr int kGatherThreads = 256;
+constexpr int kGatherR = 4;  // clients per thread
+
+template <class DistT, class OrdT>
+__global__ void __launch_bounds__(kGatherThreads)
+    k_gather(const DistT* __restrict__ dT, const OrdT* __restrict__ ord, const DistT* __restrict__ dist,
+             int n, int m, int p, int W, int Wp, const uint64_t* __restrict__ words, int wp,
+             const uint32_t* __restrict__ lists, const uint32_t* __restrict__ counts, int cap,
+             size_t count, int chunk, unsigned long long* __restrict__ costs,
+             unsigned long long* __restrict__ err, int mode) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* part = reinterpret_cast<unsigned long long*>(smem);  // [warps][chunk]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kGatherThreads / 32;
+  const size_t cbase = (size_t)blockIdx.y * chunk;
+  const int cn = (int)min((size_t)chunk, count - cbase);
+
+  int ci[kGatherR];
+  uint64_t dlast[kGatherR];
+  uint32_t jlast[kGatherR];
+#pragma unroll
+  for (int r = 0; r < kGatherR; ++r) {
+    ci[r] = blockIdx.x * kGatherThreads * kGatherR + r * kGatherThreads + tid;
+    dlast[r] = 0;
+    jlast[r] = 0;
+    if (mode == 0 && ci[r] < n) {
+      dlast[r] = (uint64_t)dist[(size_t)ci[r] * Wp + (W - 1)];
+      jlast[r] = (uint32_t)ord[(size_t)ci[r] * Wp + (W - 1)];
+    }
+  }
+  const uint64_t kMax = ~0ull;
+
+  for (int cl = 0; cl < cn; ++cl) {
+    const size_t c = cbase + cl;
+    const uint32_t pc = counts[c];
+    unsigned long long sum = 0;
+    if (pc == 0) {
+      if (tid == 0) atomicMin(err, (unsigned long long)c);
+    } else if (pc <= (uint32_t)cap && !(mode == 0 && pc < (uint32_t)p)) {
+      // common case: plain gather-min over the open list
+      uint64_t best[kGatherR];
+#pragma unroll
+      for (int r = 0; r < kGatherR; ++r) best[r] = kMax;
+      const uint32_t* list = lists + c * (size_t)cap;
+      uint32_t t = 0;
+      for (; t + 4 <= pc; t += 4) {
+        uint32_t j[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) j[x] = __ldg(list + t + x);
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int r = 0; r < kGatherR; ++r)
+            if (ci[r] < n) {
+              const uint64_t v = (uint64_t)dT[(size_t)j[x] * n + ci[r]];
+              best[r] = v < best[r] ? v : best[r];
+            }
+      }
+      for (; t < pc; ++t) {
+        const uint32_t j = __ldg(list + t);
+#pragma unroll
+        for (int r = 0; r < kGatherR; ++r)
+          if (ci[r] < n) {
+            const uint64_t v = (uint64_t)dT[(size_t)j * n + ci[r]];
+            best[r] = v < best[r] ? v : best[r];
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < kGatherR; ++r)
+        if (ci[r] < n) sum += best[r];
+    } else {
+      // general path: walk the words in site order, track the (cost, site)
+      // minimum and, under the fitness contract with fewer than p open sites,
+      // check it sorts within the first W columns (ordering.cpp:50-52).
+      uint64_t best[kGatherR];
+      uint32_t bj[kGatherR];
+#pragma unroll
+      for (int r = 0; r < kGatherR; ++r) {
+        best[r] = kMax;
+        bj[r] = 0;
+      }
+      const uint64_t* w = words + c * wp;
+      for (int wi = 0; wi < wp; ++wi) {
+        uint64_t x = __ldg(w + wi);
+        if (wi == wp - 1 && (m & 63)) x &= (1ull << (m & 63)) - 1;
+        while (x) {
+          const uint32_t j = wi * 64 + (__ffsll((long long)x) - 1);
+          x &= x - 1;
+#pragma unroll
+          for (int r = 0; r < kGatherR; ++r)
+            if (ci[r] < n) {
+              const uint64_t v = (uint64_t)dT[(size_t)j * n + ci[r]];
+              if (v < best[r]) {  // strict: ascending j keeps the lowest site on ties
+                best[r] = v;
+                bj[r] = j;
+              }
+            }
+        }
+      }
+      bool bad = false;
+#pragma unroll
+      for (int r = 0; r < kGatherR; ++r)
+        if (ci[r] < n) {
+          sum += best[r];
+          if (mode == 0 && pc < (uint32_t)p)
+            bad |= !(best[r] < dlast[r] || (best[r] == dlast[r] && bj[r] <= jlast[r]));
+        }
+      if (__any_sync(kFull, bad) && lane == 0) atomicMin(err, (unsigned long long)c);
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) part[warp * chunk + cl] = sum;
+  }
+  __syncthreads();
+  for (int cl = tid; cl < cn; cl += kGatherThreads) {
+    unsigned long long s = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += part[w * chunk + cl];
+    atomicAdd(&costs[cbase + cl], s);
+  }
+}
+
+template <class DistT, class OrdT>
+static cudaError_t launch_gather_t(const DevTables& t, const uint64_t* words, size_t count, int wp,
+                                   const uint32_t* lists, const uint32_t* counts, int cap,
+                                   unsigned long long* costs, unsigned long long* err, int mode,
+                                   int sms, cudaStream_t st) {
+  const int xblocks = (t.n + kGatherThreads * kGatherR - 1) / (kGatherThreads * kGatherR);
+  // enough CTAs for ~4 waves of 4 resident CTAs per SM
+  long long want = (long long)sms * 16;
+  int chunk = (int)std::max<long long>(1, std::min<long long>(256, (long long)count * xblocks / want));
+  const unsigned yblocks = (unsigned)((count + chunk - 1) / chunk);
+  const size_t smem = (size_t)(kGatherThreads / 32) * chunk * 8;
+  k_gather<DistT, OrdT><<<dim3(xblocks, yblocks), kGatherThreads, smem, st>>>(
+      (const DistT*)t.dT, (const OrdT*)t.ord, (const DistT*)t.dist, t.n, t.m, t.p, t.W, t.Wp, words,
+      wp, lists, counts, cap, count, chunk, costs, err, mode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_open_lists(const uint64_t* words, size_t count, int words_per, int m,
+                              uint32_t* open_lists, uint32_t* open_counts, int open_cap, cudaStream_t st) {
+  k_open_lists<<<(unsigned)((count + 7) / 8), 256, 0, st>>>(words, count, words_per, m, open_lists,
+                                                             open_counts, open_cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const DevTables& t, const uint64_t* words, size_t count, int words_per,
+                          uint32_t* open_lists, uint32_t* open_counts, int open_cap,
+                          unsigned long long* costs_acc, unsigned long long* err_first_bad, int mode,
+                          int sms, cudaStream_t st) {
+  if (t.site_bytes == 2) {
+    if (t.dist_bytes == 2) return launch_gather_t<uint16_t, uint16_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
+    if (t.dist_bytes == 4) return launch_gather_t<uint32_t, uint16_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
+    return launch_gather_t<uint64_t, uint16_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
+  }
+  if (t.dist_bytes == 2) return launch_gather_t<uint16_t, uint32_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
+  if (t.dist_bytes == 4) return launch_gather_t<uint32_t, uint32_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
+  return launch_gather_t<uint64_t, uint32_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
+}
+
+}  // namespace pmb

@@ -1,0 +1,70 @@
+// Host-side declarations of the kernel launchers (internal to libpmedian_b200).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+namespace pmb {
+
+enum class KeyKind { kPacked32, kPacked64, kPayload64 };
+
+// K1 launch plan, chosen by the host from the validated instance.
+struct BuildPlan {
+  int n = 0, m = 0, p = 0, W = 0, Wp = 0;
+  int site_bytes = 4, dist_bytes = 8;
+  int sitebits = 0, costbits = 0, npasses = 0;
+  KeyKind key_kind = KeyKind::kPacked64;
+  bool smem_path = true;
+  int grid = 0;
+};
+
+size_t sort_smem_header();
+cudaError_t launch_scan_costs(const int64_t* costs, size_t count, unsigned long long* out_max,
+                              int* out_neg, int sms, cudaStream_t st);
+cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
+                              void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st);
+cudaError_t launch_transpose_costs(const int64_t* costs, int n, int m, int dist_bytes, void* dT,
+                                   cudaStream_t st);
+
+// Device-resident tables as the evaluation kernels see them.
+struct DevTables {
+  int n = 0, m = 0, p = 0, W = 0, Wp = 0;
+  int site_bytes = 2, dist_bytes = 2;
+  int64_t max_cost = 0;
+  const void* ord = nullptr;   // n x Wp, OrdT
+  const void* dist = nullptr;  // n x Wp, DistT (sorted costs)
+  const void* dT = nullptr;    // m x n, DistT (site-major costs, gather kernel)
+};
+
+// K2t: population words -> per-group transposed site masks T[g][s] (64 chromosomes / group).
+size_t scan_t_stride(int m);  // u64 entries per group (>= m + 1, even)
+cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int words_per, int m,
+                                        uint64_t* T, cudaStream_t st);
+
+// K2: bit-sliced scan.  costs_acc (count u64) must be zeroed; err_first_bad
+// (u64) must hold ~0 before the launch.
+struct ScanPlan {
+  int warps = 8;
+  int ctas = 0;
+  bool acc32 = true;
+  size_t smem = 0;
+};
+ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode);
+// depth_mode != 0 accumulates the 1-based stopping columns k* instead of costs.
+cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* T, size_t count,
+                        unsigned long long* costs_acc, unsigned long long* err_first_bad,
+                        int depth_mode, cudaStream_t st);
+
+// K2b prep: per-chromosome open-site lists (cap entries) and popcounts.
+cudaError_t launch_open_lists(const uint64_t* words, size_t count, int words_per, int m,
+                              uint32_t* open_lists, uint32_t* open_counts, int open_cap, cudaStream_t st);
+// K2b: gather-min (needs launch_open_lists first).  mode 0 = fitness semantics (scan-width contract), 1 = min_cost_sum.
+cudaError_t launch_gather(const DevTables& t, const uint64_t* words, size_t count, int words_per,
+                          uint32_t* open_lists, uint32_t* open_counts, int open_cap,
+                          unsigned long long* costs_acc, unsigned long long* err_first_bad, int mode,
+                          int sms, cudaStream_t st);
+
+}  // namespace pmb

@@ -1,0 +1,315 @@
+// K1: device construction of the ordering tables.
+//
+// Replaces pmedian::build_ordering (/root/reference/proj/src/ordering.cpp:10-38):
+// per client row, order the sites by (cost, site index) ascending -- the
+// reference's comparator with its lower-index tie-break (ordering.cpp:25-28) --
+// and keep the first W = m - p + 1 columns (ordering.cpp:17).
+//
+// Device layout (row-major, row stride Wp = round_up(W, 16) elements):
+//   ord[i][k]  = pi_ik             (OrdT = u16 when m < 65535, else u32)
+//   dist[i][k] = cost(i, pi_ik)    (DistT = u16 / u32 / u64 by max cost)
+//   columns k in [W, Wp) hold the sentinel site m (never open) and cost 0.
+// The reference stores first differences (increments, ordering.cpp:29-35); we
+// store their prefix sums -- the sorted row itself -- because the fitness scan
+// only ever needs the prefix sum up to the stopping column, which equals
+// dist[i][k*] exactly (pinned by proj/tests/test_formulation.cpp:63-83).
+// pm_get_tables re-derives the reference's increments for parity checks.
+//
+// Algorithm: one CTA per row (persistent over rows), a stable LSD radix sort
+// over the cost bits only.  Rows start in site order and every pass is stable,
+// so equal costs keep ascending site order: exactly the reference's order.
+// Keys are packed (cost << sitebits | site) into u32 or u64 when they fit, so
+// the site rides along for free; otherwise the u64 cost is the key and the site
+// a separate payload.  Ranking within a 1024-element tile uses __match_any_sync
+// per warp plus a per-digit exclusive scan across warps.
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pmb {
+
+// ---- validation scan: max cost and negativity (instance.cpp:20-24) --------
+
+__global__ void k_scan_costs(const int64_t* __restrict__ costs, size_t count,
+                             unsigned long long* __restrict__ out_max, int* __restrict__ out_neg) {
+  int64_t mx = 0;
+  int neg = 0;
+  for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < count;
+       x += (size_t)gridDim.x * blockDim.x) {
+    const int64_t c = costs[x];
+    neg |= c < 0;
+    mx = c > mx ? c : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t v = __shfl_xor_sync(kFull, mx, o);
+    mx = v > mx ? v : mx;
+  }
+  neg = __any_sync(kFull, neg);
+  if (lane_id() == 0) {
+    atomicMax(out_max, (unsigned long long)mx);
+    if (neg) atomicOr(out_neg, 1);
+  }
+}
+
+// ---- K1: per-row stable radix sort ----------------------------------------
+
+constexpr int kSortThreads = 1024;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kHistPitch = 33;  // padded [digit][warp] so leaders of one warp hit distinct banks
+
+template <class KeyT, bool kPayload>
+__device__ __forceinline__ unsigned digit_of(KeyT key, int shift) {
+  return (unsigned)(key >> shift) & 0xffu;
+}
+
+template <class KeyT, bool kPayload, class OrdT, class DistT, bool kSmem>
+__global__ void __launch_bounds__(kSortThreads, 1)
+    k_build_rows(const int64_t* __restrict__ costs, int n, int m, int W, int Wp, int sitebits,
+                 int npasses, OrdT* __restrict__ ord, DistT* __restrict__ dist,
+                 KeyT* __restrict__ gkeys, uint32_t* __restrict__ gpay) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* bucket = reinterpret_cast<uint32_t*>(smem);  // 256
+  uint32_t* tcount = bucket + 256;                      // 256
+  uint32_t* wh = tcount + 256;                          // 256 * kHistPitch
+  int* flag = reinterpret_cast<int*>(wh + 256 * kHistPitch);
+  unsigned char* bufbase = smem + ((256 + 256 + 256 * kHistPitch + 4) * 4 + 15) / 16 * 16;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  KeyT *A, *B;
+  uint32_t *PA = nullptr, *PB = nullptr;
+  if constexpr (kSmem) {
+    A = reinterpret_cast<KeyT*>(bufbase);
+    B = A + m;
+    if constexpr (kPayload) {
+      PA = reinterpret_cast<uint32_t*>(B + m);
+      PB = PA + m;
+    }
+  } else {
+    A = gkeys + (size_t)blockIdx.x * 2 * m;
+    B = A + m;
+    if constexpr (kPayload) {
+      PA = gpay + (size_t)blockIdx.x * 2 * m;
+      PB = PA + m;
+    }
+  }
+  const unsigned lt = lanemask_lt();
+  const KeyT sitemask = kPayload ? KeyT(0) : ((KeyT(1) << sitebits) - 1);
+  const int shift0 = kPayload ? 0 : sitebits;
+
+  for (int x = tid; x < 256 * kHistPitch; x += kSortThreads) wh[x] = 0;
+
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int64_t* crow = costs + (size_t)r * m;
+    KeyT* src = A;
+    KeyT* dst = B;
+    uint32_t* psrc = PA;
+    uint32_t* pdst = PB;
+    if (tid < 256) bucket[tid] = 0;
+    __syncthreads();
+    for (int x = tid; x < m; x += kSortThreads) {
+      const uint64_t c = (uint64_t)crow[x];
+      KeyT key;
+      if constexpr (kPayload) {
+        key = (KeyT)c;
+        psrc[x] = (uint32_t)x;
+      } else {
+        key = ((KeyT)c << sitebits) | (KeyT)x;
+      }
+      src[x] = key;
+      if (npasses > 0) atomicAdd(&bucket[digit_of<KeyT, kPayload>(key, shift0)], 1u);
+    }
+    __syncthreads();
+
+    for (int q = 0; q < npasses; ++q) {
+      const int shift = shift0 + 8 * q;
+      if (q > 0) {
+        if (tid < 256) bucket[tid] = 0;
+        __syncthreads();
+        for (int x = tid; x < m; x += kSortThreads)
+          atomicAdd(&bucket[digit_of<KeyT, kPayload>(src[x], shift)], 1u);
+        __syncthreads();
+      }
+      // A pass whose digit is constant over the row is the identity: skip it.
+      const bool skip = bucket[digit_of<KeyT, kPayload>(src[0], shift)] == (uint32_t)m;
+      if (skip) continue;  // uniform across the CTA
+      if (warp == 0) {     // exclusive scan of the 256 digit counts
+        uint32_t v[8], s = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[j] = bucket[lane * 8 + j];
+          s += v[j];
+        }
+        uint32_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += t;
+        }
+        uint32_t run = incl - s;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          bucket[lane * 8 + j] = run;
+          run += v[j];
+        }
+      }
+      __syncthreads();
+
+      for (int t0 = 0; t0 < m; t0 += kSortThreads) {
+        const int x = t0 + tid;
+        const bool valid = x < m;
+        const KeyT key = valid ? src[x] : KeyT(0);
+        const uint32_t pay = (kPayload && valid) ? psrc[x] : 0u;
+        const unsigned d = valid ? digit_of<KeyT, kPayload>(key, shift) : 256u;
+        const unsigned peers = __match_any_sync(kFull, d);
+        const unsigned rank = __popc(peers & lt);
+        if (valid && rank == 0) wh[d * kHistPitch + warp] = __popc(peers);
+        __syncthreads();
+        // per digit: exclusive prefix over warps (warp w owns digits w, w+32, ...)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int dd = warp + 32 * j;
+          const uint32_t v = wh[dd * kHistPitch + lane];
+          uint32_t incl = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+          }
+          wh[dd * kHistPitch + lane] = incl - v;
+          if (lane == 31) tcount[dd] = incl;
+        }
+        __syncthreads();
+        if (valid) {
+          const uint32_t pos = bucket[d] + wh[d * kHistPitch + warp] + rank;
+          dst[pos] = key;
+          if constexpr (kPayload) pdst[pos] = pay;
+        }
+        __syncthreads();
+        if (valid && rank == 0) wh[d * kHistPitch + warp] = 0;
+        if (tid < 256) bucket[tid] += tcount[tid];
+      }
+      __syncthreads();
+      KeyT* tk = src;
+      src = dst;
+      dst = tk;
+      uint32_t* tp = psrc;
+      psrc = pdst;
+      pdst = tp;
+    }
+
+    OrdT* orow = ord + (size_t)r * Wp;
+    DistT* drow = dist + (size_t)r * Wp;
+    for (int k = tid; k < Wp; k += kSortThreads) {
+      if (k < W) {
+        const KeyT key = src[k];
+        uint32_t site;
+        uint64_t d;
+        if constexpr (kPayload) {
+          site = psrc[k];
+          d = (uint64_t)key;
+        } else {
+          site = (uint32_t)(key & sitemask);
+          d = (uint64_t)(key >> sitebits);
+        }
+        orow[k] = (OrdT)site;
+        drow[k] = (DistT)d;
+      } else {
+        orow[k] = (OrdT)m;  // sentinel: T[m] == 0, never open
+        drow[k] = (DistT)0;
+      }
+    }
+    __syncthreads();
+    (void)flag;
+  }
+}
+
+// ---- site-major narrow cost matrix for the gather-min kernel (K2b) --------
+
+template <class DistT>
+__global__ void k_transpose_costs(const int64_t* __restrict__ costs, int n, int m,
+                                  DistT* __restrict__ dT) {
+  __shared__ int64_t tile[32][33];
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + tx;
+    if (i < n && j < m) tile[r][tx] = costs[(size_t)i * m + j];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int j = j0 + r, i = i0 + tx;
+    if (i < n && j < m) dT[(size_t)j * n + i] = (DistT)tile[tx][r];
+  }
+}
+
+// ---- host launchers --------------------------------------------------------
+
+cudaError_t launch_scan_costs(const int64_t* costs, size_t count, unsigned long long* out_max,
+                              int* out_neg, int sms, cudaStream_t st) {
+  const int blocks = (int)std::min<size_t>((size_t)sms * 8, (count + 255) / 256 + 1);
+  k_scan_costs<<<blocks, 256, 0, st>>>(costs, count, out_max, out_neg);
+  return cudaGetLastError();
+}
+
+size_t sort_smem_header() { return ((256 + 256 + 256 * kHistPitch + 4) * 4 + 15) / 16 * 16; }
+
+template <class KeyT, bool kPayload, class OrdT, class DistT>
+static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
+                                 void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st) {
+  const size_t per = (size_t)bp.m * (sizeof(KeyT) + (kPayload ? 4 : 0)) * 2;
+  const size_t smem = sort_smem_header() + per;
+  if (bp.smem_path) {
+    auto kern = k_build_rows<KeyT, kPayload, OrdT, DistT, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<bp.grid, kSortThreads, smem, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits,
+                                              bp.npasses, (OrdT*)ord, (DistT*)dist, nullptr, nullptr);
+  } else {
+    auto kern = k_build_rows<KeyT, kPayload, OrdT, DistT, false>;
+    const size_t hs = sort_smem_header();
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
+    if (e != cudaSuccess) return e;
+    kern<<<bp.grid, kSortThreads, hs, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits,
+                                            bp.npasses, (OrdT*)ord, (DistT*)dist,
+                                            (KeyT*)scratch_keys, scratch_pay);
+  }
+  return cudaGetLastError();
+}
+
+template <class OrdT, class DistT>
+static cudaError_t launch_rows_od(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
+                                  void* sk, uint32_t* sp, cudaStream_t st) {
+  switch (bp.key_kind) {
+    case KeyKind::kPacked32:
+      return launch_rows_t<uint32_t, false, OrdT, DistT>(bp, costs, ord, dist, sk, sp, st);
+    case KeyKind::kPacked64:
+      return launch_rows_t<uint64_t, false, OrdT, DistT>(bp, costs, ord, dist, sk, sp, st);
+    default:
+      return launch_rows_t<uint64_t, true, OrdT, DistT>(bp, costs, ord, dist, sk, sp, st);
+  }
+}
+
+cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
+                              void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st) {
+  if (bp.site_bytes == 2) {
+    if (bp.dist_bytes == 2) return launch_rows_od<uint16_t, uint16_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
+    if (bp.dist_bytes == 4) return launch_rows_od<uint16_t, uint32_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
+    return launch_rows_od<uint16_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
+  }
+  if (bp.dist_bytes == 2) return launch_rows_od<uint32_t, uint16_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
+  if (bp.dist_bytes == 4) return launch_rows_od<uint32_t, uint32_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
+  return launch_rows_od<uint32_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
+}
+
+cudaError_t launch_transpose_costs(const int64_t* costs, int n, int m, int dist_bytes, void* dT,
+                                   cudaStream_t st) {
+  dim3 grid((m + 31) / 32, (n + 31) / 32), block(32, 8);
+  if (dist_bytes == 2) k_transpose_costs<uint16_t><<<grid, block, 0, st>>>(costs, n, m, (uint16_t*)dT);
+  else if (dist_bytes == 4) k_transpose_costs<uint32_t><<<grid, block, 0, st>>>(costs, n, m, (uint32_t*)dT);
+  else k_transpose_costs<uint64_t><<<grid, block, 0, st>>>(costs, n, m, (uint64_t*)dT);
+  return cudaGetLastError();
+}
+
+}  // namespace pmb
