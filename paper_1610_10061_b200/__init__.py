@@ -171,7 +171,12 @@ class Context:
 
     def set_stream(self, stream) -> None:
         """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""
-        handle = None if stream is None else int(getattr(stream, "cuda_stream", stream))
+        if stream is None:
+            handle = None  # the context's own stream
+        else:
+            handle = int(getattr(stream, "cuda_stream", stream))
+            if handle == 0:
+                handle = 1  # torch's default stream is the legacy NULL stream: cudaStreamLegacy
         self._check(_lib.pm_set_stream(self._h, handle))
 
     def set_eval_kernel(self, kind: int) -> None:

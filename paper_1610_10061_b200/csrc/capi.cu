@@ -247,7 +247,7 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
 
 int pm_set_instance(pm_ctx* c, const int64_t* costs, size_t n, size_t m, size_t p) {
   if (!c) return PM_STRUCTURAL;
-  if (!costs && n * m) return c->fail(PM_STRUCTURAL, "cost matrix must be exactly n rows by m columns");
+  if (!costs && n != 0 && m != 0) return c->fail(PM_STRUCTURAL, "cost matrix must be exactly n rows by m columns");
   PM_CUDA_TRY(c, cudaSetDevice(c->device));
   if (n == 0 || m == 0 || p < 1 || p >= m) return set_instance_impl(c, nullptr, n, m, p);
   PM_CUDA_TRY(c, c->costs_in.ensure(n * m * 8));

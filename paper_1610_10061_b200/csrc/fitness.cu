@@ -106,7 +106,9 @@ struct Chunk {
   }
 };
 
-template <class OrdT, class DistT, class AccT>
+// kTSmem: the group's masks T live in shared memory (m up to ~26k); otherwise
+// they are read from global memory through L1/L2 (any m).
+template <class OrdT, class DistT, class AccT, bool kTSmem>
 __global__ void __launch_bounds__(512, 1)
     k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
            const uint64_t* __restrict__ T, size_t Ts, size_t count, int groups,
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(512, 1)
   extern __shared__ __align__(16) unsigned char smem[];
   const int nwarps = blockDim.x >> 5;
   uint64_t* Tsm = reinterpret_cast<uint64_t*>(smem);
-  AccT* acc = reinterpret_cast<AccT*>(smem + Ts * 8);
+  AccT* acc = reinterpret_cast<AccT*>(smem + (kTSmem ? Ts * 8 : 0));
   unsigned long long* red = reinterpret_cast<unsigned long long*>(acc + (size_t)nwarps * 64 * 32);
   int* next_client = reinterpret_cast<int*>(red + (nwarps / 2) * 64);
 
@@ -133,13 +135,16 @@ __global__ void __launch_bounds__(512, 1)
     u += c1 - c0;
 
     {  // stage the group's masks, clear the counters
-      const uint4* src = reinterpret_cast<const uint4*>(T + (size_t)g * Ts);
-      uint4* dstT = reinterpret_cast<uint4*>(Tsm);
-      for (size_t x = tid; x < Ts / 2; x += blockDim.x) dstT[x] = src[x];
+      if constexpr (kTSmem) {
+        const uint4* src = reinterpret_cast<const uint4*>(T + (size_t)g * Ts);
+        uint4* dstT = reinterpret_cast<uint4*>(Tsm);
+        for (size_t x = tid; x < Ts / 2; x += blockDim.x) dstT[x] = src[x];
+      }
       for (int x = tid; x < nwarps * 64 * 32; x += blockDim.x) acc[x] = 0;
       if (tid == 0) *next_client = c0;
     }
     __syncthreads();
+    const uint64_t* Tlook = kTSmem ? Tsm : T + (size_t)g * Ts;
     const size_t nvalid = min((size_t)64, count - (size_t)g * 64);
     const uint64_t vmask = nvalid == 64 ? ~0ull : ((1ull << nvalid) - 1);
 
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(512, 1)
       if (i >= 0) {
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
-          const uint64_t t = Tsm[cur.site(j)];
+          const uint64_t t = kTSmem ? Tlook[cur.site(j)] : __ldg(Tlook + cur.site(j));
           uint64_t h = alive & t;
           alive &= ~t;
           if (h) {
@@ -229,30 +234,36 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
-static size_t scan_smem(int m, int warps, bool acc32) {
-  return scan_t_stride(m) * 8 + (size_t)warps * 64 * 32 * (acc32 ? 4 : 8) + (warps / 2) * 64 * 8 + 16;
+static size_t scan_smem(int m, int warps, bool acc32, bool tsmem) {
+  return (tsmem ? scan_t_stride(m) * 8 : 0) + (size_t)warps * 64 * 32 * (acc32 ? 4 : 8) + (warps / 2) * 64 * 8 + 16;
 }
 
 template <class OrdT, class DistT, class AccT>
-static const void* scan_fn() {
-  return reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT>);
+static const void* scan_fn_acc(bool tsmem) {
+  return tsmem ? reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT, true>)
+               : reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT, false>);
 }
 
-static const void* scan_kernel_ptr(const DevTables& t, bool acc32) {
+static const void* scan_kernel_ptr(const DevTables& t, bool acc32, bool ts) {
   if (t.site_bytes == 2) {
-    if (t.dist_bytes == 2) return acc32 ? scan_fn<uint16_t, uint16_t, uint32_t>() : scan_fn<uint16_t, uint16_t, uint64_t>();
-    if (t.dist_bytes == 4) return acc32 ? scan_fn<uint16_t, uint32_t, uint32_t>() : scan_fn<uint16_t, uint32_t, uint64_t>();
-    return acc32 ? scan_fn<uint16_t, uint64_t, uint32_t>() : scan_fn<uint16_t, uint64_t, uint64_t>();
+    if (t.dist_bytes == 2) return acc32 ? scan_fn_acc<uint16_t, uint16_t, uint32_t>(ts) : scan_fn_acc<uint16_t, uint16_t, uint64_t>(ts);
+    if (t.dist_bytes == 4) return acc32 ? scan_fn_acc<uint16_t, uint32_t, uint32_t>(ts) : scan_fn_acc<uint16_t, uint32_t, uint64_t>(ts);
+    return acc32 ? scan_fn_acc<uint16_t, uint64_t, uint32_t>(ts) : scan_fn_acc<uint16_t, uint64_t, uint64_t>(ts);
   }
-  if (t.dist_bytes == 2) return acc32 ? scan_fn<uint32_t, uint16_t, uint32_t>() : scan_fn<uint32_t, uint16_t, uint64_t>();
-  if (t.dist_bytes == 4) return acc32 ? scan_fn<uint32_t, uint32_t, uint32_t>() : scan_fn<uint32_t, uint32_t, uint64_t>();
-  return acc32 ? scan_fn<uint32_t, uint64_t, uint32_t>() : scan_fn<uint32_t, uint64_t, uint64_t>();
+  if (t.dist_bytes == 2) return acc32 ? scan_fn_acc<uint32_t, uint16_t, uint32_t>(ts) : scan_fn_acc<uint32_t, uint16_t, uint64_t>(ts);
+  if (t.dist_bytes == 4) return acc32 ? scan_fn_acc<uint32_t, uint32_t, uint32_t>(ts) : scan_fn_acc<uint32_t, uint32_t, uint64_t>(ts);
+  return acc32 ? scan_fn_acc<uint32_t, uint64_t, uint32_t>(ts) : scan_fn_acc<uint32_t, uint64_t, uint64_t>(ts);
 }
 
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode) {
   ScanPlan sp;
   const size_t groups = (count + 63) / 64;
-  for (int warps : {16, 8, 4}) {
+  // (warps, masks in smem?) in preference order; the last entry reads the
+  // masks from global memory and always fits.
+  const std::pair<int, bool> shapes[] = {{16, true}, {8, true}, {4, true}, {16, false}};
+  for (const auto& shape : shapes) {
+    const int warps = shape.first;
+    const bool tsmem = shape.second;
     for (int pass = 0; pass < 2; ++pass) {
       const int blocks_per_sm = 1;
       const int ctas = sms * blocks_per_sm;
@@ -263,8 +274,9 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
       const bool acc32 =
           pass == 0 && (unsigned long long)std::min<long long>(seg, t.n) * vmax < (1ull << 32);
       if (pass == 0 && !acc32) continue;
-      const size_t smem = scan_smem(t.m, warps, acc32);
+      const size_t smem = scan_smem(t.m, warps, acc32, tsmem);
       if (smem <= max_smem) {
+        sp.tsmem = tsmem;
         sp.warps = warps;
         sp.acc32 = acc32;
         sp.smem = smem;
@@ -280,7 +292,7 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
 cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* T, size_t count,
                         unsigned long long* costs_acc, unsigned long long* err_first_bad,
                         int depth_mode, cudaStream_t st) {
-  const void* fn = scan_kernel_ptr(t, sp.acc32);
+  const void* fn = scan_kernel_ptr(t, sp.acc32, sp.tsmem);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem);
   if (e != cudaSuccess) return e;
   const int groups = (int)((count + 63) / 64);

@@ -50,6 +50,7 @@ struct ScanPlan {
   int warps = 8;
   int ctas = 0;
   bool acc32 = true;
+  bool tsmem = true;  // masks staged in shared memory (else read from global)
   size_t smem = 0;
 };
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode);

@@ -56,7 +56,7 @@ __global__ void k_scan_costs(const int64_t* __restrict__ costs, size_t count,
 // ---- K1: per-row stable radix sort ----------------------------------------
 
 constexpr int kSortThreads = 1024;
-constexpr int kSortWarps = kSortThreads / 32;
+static_assert(kSortThreads == 1024, "the digit scan assumes 32 warps");
 constexpr int kHistPitch = 33;  // padded [digit][warp] so leaders of one warp hit distinct banks
 
 template <class KeyT, bool kPayload>
@@ -187,7 +187,10 @@ __global__ void __launch_bounds__(kSortThreads, 1)
           if constexpr (kPayload) pdst[pos] = pay;
         }
         __syncthreads();
-        if (valid && rank == 0) wh[d * kHistPitch + warp] = 0;
+        // the scan wrote prefixes into every (digit, warp) cell: clear the
+        // cells this warp scanned so the next tile starts from zero counts
+#pragma unroll
+        for (int j = 0; j < 8; ++j) wh[(warp + 32 * j) * kHistPitch + lane] = 0;
         if (tid < 256) bucket[tid] += tcount[tid];
       }
       __syncthreads();
