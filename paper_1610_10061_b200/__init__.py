@@ -142,9 +142,9 @@ class Context:
         self.m = self.n = self.p = None
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.pm_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         self.close()

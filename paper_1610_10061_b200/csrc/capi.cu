@@ -171,7 +171,7 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   PM_CUDA_TRY(c, c->scal.ensure(16));
   scal = c->scal.as<unsigned long long>();
   PM_CUDA_TRY(c, cudaMemsetAsync(scal, 0, 16, c->stream));
-  PM_CUDA_TRY(c, launch_scan_costs(dcosts, n * m, scal, reinterpret_cast<int*>(scal + 1), c->sms,
+  PM_CUDA_TRY(c, launch_validate_costs(dcosts, n * m, scal, reinterpret_cast<int*>(scal + 1), c->sms,
                                    c->stream));
   c->launches += 1;
   unsigned long long host[2] = {0, 0};

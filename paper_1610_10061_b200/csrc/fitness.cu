@@ -26,6 +26,8 @@
 // (W = m-p+1 columns always contain one of p distinct sites); with fewer open
 // sites the (cost, site)-smallest open site must not sort after column W-1.
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -106,24 +108,64 @@ struct Chunk {
   }
 };
 
-// kTSmem: the group's masks T live in shared memory (m up to ~26k); otherwise
-// they are read from global memory through L1/L2 (any m).
-template <class OrdT, class DistT, class AccT, bool kTSmem>
+// Group width: MaskT = uint64_t (64 chromosomes per row walk) or uint32_t (32).
+// Wider groups amortise a row walk over more evaluations (E[max k*] grows only
+// like H_G) but need twice the shared memory per site and per lane counter;
+// plan_scan picks the width that keeps enough warps resident.
+template <class MaskT>
+struct MaskOps {
+  static constexpr int kG = 8 * sizeof(MaskT);
+  __device__ __forceinline__ static int pop_high(MaskT& h) {  // index of the top set bit, cleared
+    if constexpr (sizeof(MaskT) == 4) {
+      const int c = 31 - __clz(h);
+      h ^= 1u << c;
+      return c;
+    } else {
+      const int c = 63 - __clzll((long long)h);
+      h ^= 1ull << c;
+      return c;
+    }
+  }
+  __device__ __forceinline__ static int low_index(MaskT h) {
+    return sizeof(MaskT) == 4 ? __ffs((int)h) - 1 : __ffsll((long long)h) - 1;
+  }
+};
+
+// kTSmem: the group's masks T live in shared memory; otherwise they are read
+// from global memory through L1/L2 (any m).
+//
+// Per chunk of 16 columns a lane (1) looks up the 16 masks, (2) walks them to
+// update `alive`, parking each column's newly-dead chromosomes h_j and the
+// column's cost in a per-lane shared-memory slot (predicated stores), and (3)
+// drains the parked hits in one loop whose trip count is the lane's hit count
+// for the whole chunk, into per-lane private counters acc[c][lane] (no
+// atomics, no bank conflicts).  Draining per chunk instead of per column keeps
+// the warp converged: the loop runs max_lane(hits in chunk) times, not
+// sum_j max_lane(hits in column j).
+template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kDepth>
 __global__ void __launch_bounds__(512, 1)
     k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
            const uint64_t* __restrict__ T, size_t Ts, size_t count, int groups,
-           unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err,
-           int depth_mode) {
+           unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err) {
+  using Ops = MaskOps<MaskT>;
+  constexpr int kG = Ops::kG;
+  // row chunks in registers: 3 (two in flight while one is consumed) when the
+  // table types are narrow, else 2 to stay within the register budget
+  constexpr int kBufs = sizeof(OrdT) + sizeof(DistT) <= 4 ? 3 : 2;
   extern __shared__ __align__(16) unsigned char smem[];
   const int nwarps = blockDim.x >> 5;
-  uint64_t* Tsm = reinterpret_cast<uint64_t*>(smem);
-  AccT* acc = reinterpret_cast<AccT*>(smem + (kTSmem ? Ts * 8 : 0));
-  unsigned long long* red = reinterpret_cast<unsigned long long*>(acc + (size_t)nwarps * 64 * 32);
-  int* next_client = reinterpret_cast<int*>(red + (nwarps / 2) * 64);
+  MaskT* Tsm = reinterpret_cast<MaskT*>(smem);
+  const size_t tbytes = kTSmem ? (Ts * sizeof(MaskT) + 15) / 16 * 16 : 0;
+  AccT* acc = reinterpret_cast<AccT*>(smem + tbytes);                              // [warp][c][lane]
+  MaskT* hbuf = reinterpret_cast<MaskT*>(acc + (size_t)nwarps * kG * 32);           // [warp][j][lane]
+  AccT* dbuf = reinterpret_cast<AccT*>(hbuf + (size_t)nwarps * kChunk * 32);       // [warp][j][lane]
+  int* next_client = reinterpret_cast<int*>(dbuf + (size_t)nwarps * kChunk * 32);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = lanemask_lt();
-  AccT* myacc = acc + (size_t)warp * 64 * 32 + lane;
+  AccT* myacc = acc + (size_t)warp * kG * 32 + lane;
+  MaskT* myh = hbuf + (size_t)warp * kChunk * 32 + lane;
+  AccT* myd = dbuf + (size_t)warp * kChunk * 32 + lane;
 
   const long long U = (long long)groups * n;
   long long u = U * blockIdx.x / gridDim.x;
@@ -133,31 +175,42 @@ __global__ void __launch_bounds__(512, 1)
     const int c0 = (int)(u % n);
     const int c1 = (int)min((long long)n, c0 + (uend - u));
     u += c1 - c0;
+    // T is stored as 64-chromosome words; a 32-wide group is one half of one
+    const uint64_t* Tg = T + (size_t)(g * kG / 64) * Ts;
+    const int half = (kG == 32) ? (g & 1) * 32 : 0;
 
     {  // stage the group's masks, clear the counters
       if constexpr (kTSmem) {
-        const uint4* src = reinterpret_cast<const uint4*>(T + (size_t)g * Ts);
-        uint4* dstT = reinterpret_cast<uint4*>(Tsm);
-        for (size_t x = tid; x < Ts / 2; x += blockDim.x) dstT[x] = src[x];
+        if constexpr (kG == 64) {
+          const uint4* src = reinterpret_cast<const uint4*>(Tg);
+          uint4* dstT = reinterpret_cast<uint4*>(Tsm);
+          for (size_t x = tid; x < Ts / 2; x += blockDim.x) dstT[x] = src[x];
+        } else {
+          for (size_t x = tid; x < Ts; x += blockDim.x) Tsm[x] = (MaskT)(Tg[x] >> half);
+        }
       }
-      for (int x = tid; x < nwarps * 64 * 32; x += blockDim.x) acc[x] = 0;
+      for (int x = tid; x < nwarps * kG * 32; x += blockDim.x) acc[x] = 0;
       if (tid == 0) *next_client = c0;
     }
     __syncthreads();
-    const uint64_t* Tlook = kTSmem ? Tsm : T + (size_t)g * Ts;
-    const size_t nvalid = min((size_t)64, count - (size_t)g * 64);
-    const uint64_t vmask = nvalid == 64 ? ~0ull : ((1ull << nvalid) - 1);
+    const size_t nvalid = min((size_t)kG, count - (size_t)g * kG);
+    const MaskT vmask = nvalid == (size_t)kG ? (MaskT)~(MaskT)0 : (MaskT)((((MaskT)1) << nvalid) - 1);
 
     int i = -1, k = 0;
-    uint64_t alive = 0;
+    MaskT alive = 0;
     const OrdT* orow = nullptr;
     const DistT* drow = nullptr;
-    Chunk<OrdT, DistT> cur, nxt;
+    Chunk<OrdT, DistT> ca, cb, cc;
     int wb_next = 0, wb_end = 0;
     bool exhausted = false;
-    while (true) {
+
+    // One 16-column step on chunk `cur`; `nxt` already holds the following
+    // chunk and `cur` is refilled with the one after it.  Returns false once
+    // the warp has no client left.
+    auto step = [&](Chunk<OrdT, DistT>& cur, Chunk<OrdT, DistT>& nxt,
+                    Chunk<OrdT, DistT>& nxt2) -> bool {
       unsigned need = __ballot_sync(kFull, i < 0);
-      while (need && !exhausted) {
+      while (need && !exhausted) {  // warp-uniform client claiming
         if (wb_next >= wb_end) {
           int base = 0;
           if (lane == 0) base = atomicAdd(next_client, 32);
@@ -179,105 +232,149 @@ __global__ void __launch_bounds__(512, 1)
           drow = dist + (size_t)i * Wp;
           cur.load(orow, drow, 0);
           if (kChunk < Wp) nxt.load(orow, drow, kChunk);
+          if (kBufs == 3 && 2 * kChunk < Wp) nxt2.load(orow, drow, 2 * kChunk);
         }
         wb_next += min(__popc(need), avail);
         need = __ballot_sync(kFull, i < 0);
       }
-      if (__ballot_sync(kFull, i >= 0) == 0) break;
+      if (__ballot_sync(kFull, i >= 0) == 0) return false;
       if (i >= 0) {
+        MaskT t[kChunk];
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
-          const uint64_t t = kTSmem ? Tlook[cur.site(j)] : __ldg(Tlook + cur.site(j));
-          uint64_t h = alive & t;
-          alive &= ~t;
+          if constexpr (kTSmem) t[j] = Tsm[cur.site(j)];
+          else t[j] = (MaskT)(__ldg(Tg + cur.site(j)) >> half);
+        }
+        uint32_t colmask = 0;
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const MaskT h = alive & t[j];
+          alive &= ~t[j];
           if (h) {
-            // depth_mode: accumulate the 1-based stopping column k* instead of
-            // the cost (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
-            const AccT dv = depth_mode ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
-            do {
-              const int c = __ffsll((long long)h) - 1;
-              h &= h - 1;
-              myacc[c * 32] += dv;
-            } while (h);
+            // kDepth: the 1-based stopping column k* instead of the cost
+            // (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
+            myh[j * 32] = h;
+            myd[j * 32] = kDepth ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
+            colmask |= 1u << j;
           }
+        }
+        MaskT h = 0;
+        AccT dv = 0;
+        while (colmask | (h != 0)) {
+          if (h == 0) {
+            const int j = __ffs(colmask) - 1;
+            colmask &= colmask - 1;
+            h = myh[j * 32];
+            dv = myd[j * 32];
+          }
+          const int c = Ops::pop_high(h);
+          myacc[c * 32] += dv;
         }
         k += kChunk;
         if (alive == 0 || k >= Wp) {
-          if (alive) atomicMin(err, (unsigned long long)g * 64 + (__ffsll((long long)alive) - 1));
+          if (alive) atomicMin(err, (unsigned long long)g * kG + Ops::low_index(alive));
           i = -1;
-        } else {
-          cur = nxt;
-          if (k + kChunk < Wp) nxt.load(orow, drow, k + kChunk);
+        } else if (k + (kBufs - 1) * kChunk < Wp) {
+          cur.load(orow, drow, k + (kBufs - 1) * kChunk);
         }
+      }
+      return true;
+    };
+    if constexpr (kBufs == 3) {
+      while (step(ca, cb, cc) && step(cb, cc, ca) && step(cc, ca, cb)) {
+      }
+    } else {
+      while (step(ca, cb, cb) && step(cb, ca, ca)) {
       }
     }
     __syncthreads();
-    {  // reduce the per-lane counters: thread -> (chromosome c, warp pair q)
-      const int c = tid & 63, q = tid >> 6;
+    for (int c = tid; c < (int)nvalid; c += blockDim.x) {  // chromosome c: sum every lane's counter
       unsigned long long s = 0;
-      if (q < nwarps / 2) {
-        for (int w = 2 * q; w < 2 * q + 2; ++w) {
-          const AccT* a = acc + ((size_t)w * 64 + c) * 32;
+      for (int w = 0; w < nwarps; ++w) {
+        const AccT* a = acc + ((size_t)w * kG + c) * 32;
 #pragma unroll 8
-          for (int l = 0; l < 32; ++l) s += (unsigned long long)a[(l + c) & 31];
-        }
-        red[q * 64 + c] = s;
+        for (int l = 0; l < 32; ++l) s += (unsigned long long)a[(l + c) & 31];
       }
-    }
-    __syncthreads();
-    if (tid < 64 && (size_t)tid < nvalid) {
-      unsigned long long s = 0;
-      for (int q = 0; q < nwarps / 2; ++q) s += red[q * 64 + tid];
-      atomicAdd(&costs[(size_t)g * 64 + tid], s);
+      atomicAdd(&costs[(size_t)g * kG + c], s);
     }
     __syncthreads();
   }
 }
 
-static size_t scan_smem(int m, int warps, bool acc32, bool tsmem) {
-  return (tsmem ? scan_t_stride(m) * 8 : 0) + (size_t)warps * 64 * 32 * (acc32 ? 4 : 8) + (warps / 2) * 64 * 8 + 16;
+static size_t scan_smem(int m, int warps, bool acc32, bool tsmem, int G) {
+  const size_t ab = acc32 ? 4 : 8, mb = G / 8;
+  const size_t tb = tsmem ? (scan_t_stride(m) * mb + 15) / 16 * 16 : 0;
+  return tb + (size_t)warps * 32 * (G * ab + kChunk * (mb + ab)) + 16;
 }
+
+template <class OrdT, class DistT, class AccT, bool kDepth>
+static const void* scan_fn_depth(int G, bool tsmem) {
+  if (G == 64)
+    return tsmem ? reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT, uint64_t, true, kDepth>)
+                 : reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT, uint64_t, false, kDepth>);
+  return tsmem ? reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT, uint32_t, true, kDepth>)
+               : reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT, uint32_t, false, kDepth>);
+}
+
+static thread_local bool g_depth = false;  // selects the kDepth instantiation in scan_kernel_ptr
 
 template <class OrdT, class DistT, class AccT>
-static const void* scan_fn_acc(bool tsmem) {
-  return tsmem ? reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT, true>)
-               : reinterpret_cast<const void*>(k_scan<OrdT, DistT, AccT, false>);
+static const void* scan_fn_acc(int G, bool tsmem) {
+  return g_depth ? scan_fn_depth<OrdT, DistT, AccT, true>(G, tsmem)
+                 : scan_fn_depth<OrdT, DistT, AccT, false>(G, tsmem);
 }
 
-static const void* scan_kernel_ptr(const DevTables& t, bool acc32, bool ts) {
+static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool ts) {
   if (t.site_bytes == 2) {
-    if (t.dist_bytes == 2) return acc32 ? scan_fn_acc<uint16_t, uint16_t, uint32_t>(ts) : scan_fn_acc<uint16_t, uint16_t, uint64_t>(ts);
-    if (t.dist_bytes == 4) return acc32 ? scan_fn_acc<uint16_t, uint32_t, uint32_t>(ts) : scan_fn_acc<uint16_t, uint32_t, uint64_t>(ts);
-    return acc32 ? scan_fn_acc<uint16_t, uint64_t, uint32_t>(ts) : scan_fn_acc<uint16_t, uint64_t, uint64_t>(ts);
+    if (t.dist_bytes == 2) return acc32 ? scan_fn_acc<uint16_t, uint16_t, uint32_t>(G, ts) : scan_fn_acc<uint16_t, uint16_t, uint64_t>(G, ts);
+    if (t.dist_bytes == 4) return acc32 ? scan_fn_acc<uint16_t, uint32_t, uint32_t>(G, ts) : scan_fn_acc<uint16_t, uint32_t, uint64_t>(G, ts);
+    return acc32 ? scan_fn_acc<uint16_t, uint64_t, uint32_t>(G, ts) : scan_fn_acc<uint16_t, uint64_t, uint64_t>(G, ts);
   }
-  if (t.dist_bytes == 2) return acc32 ? scan_fn_acc<uint32_t, uint16_t, uint32_t>(ts) : scan_fn_acc<uint32_t, uint16_t, uint64_t>(ts);
-  if (t.dist_bytes == 4) return acc32 ? scan_fn_acc<uint32_t, uint32_t, uint32_t>(ts) : scan_fn_acc<uint32_t, uint32_t, uint64_t>(ts);
-  return acc32 ? scan_fn_acc<uint32_t, uint64_t, uint32_t>(ts) : scan_fn_acc<uint32_t, uint64_t, uint64_t>(ts);
+  if (t.dist_bytes == 2) return acc32 ? scan_fn_acc<uint32_t, uint16_t, uint32_t>(G, ts) : scan_fn_acc<uint32_t, uint16_t, uint64_t>(G, ts);
+  if (t.dist_bytes == 4) return acc32 ? scan_fn_acc<uint32_t, uint32_t, uint32_t>(G, ts) : scan_fn_acc<uint32_t, uint32_t, uint64_t>(G, ts);
+  return acc32 ? scan_fn_acc<uint32_t, uint64_t, uint32_t>(G, ts) : scan_fn_acc<uint32_t, uint64_t, uint64_t>(G, ts);
 }
 
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode) {
   ScanPlan sp;
-  const size_t groups = (count + 63) / 64;
-  // (warps, masks in smem?) in preference order; the last entry reads the
-  // masks from global memory and always fits.
-  const std::pair<int, bool> shapes[] = {{16, true}, {8, true}, {4, true}, {16, false}};
-  for (const auto& shape : shapes) {
-    const int warps = shape.first;
-    const bool tsmem = shape.second;
+  // (group width, warps, masks in smem?) in preference order.  Measured on
+  // B200 (profiles/): 32-wide groups beat 64-wide at every BASELINE shape
+  // (64-wide doubles the mask and counter footprint and the per-lane hit
+  // bursts), and a CTA must leave L1 room for the lanes' in-flight row
+  // prefetches -- shared memory above ~200 KB halves throughput.  The last
+  // entry reads the masks from global memory and always fits.
+  const struct { int G, warps; bool tsmem; } shapes[] = {
+      {32, 16, true}, {32, 14, true}, {32, 12, true}, {32, 10, true}, {32, 8, true},
+      {32, 6, true},  {32, 4, true},  {32, 8, false}};
+  const size_t chunk_bytes = (size_t)kChunk * (t.site_bytes + t.dist_bytes);
+  const size_t l1_total = 228 * 1024;
+  const int ctas = sms;
+  const unsigned long long vmax = depth_mode ? (unsigned long long)t.Wp : (unsigned long long)t.max_cost;
+  // PMB_SCAN_SHAPE="G,warps" pins the shape (tuning experiments only)
+  const char* force = getenv("PMB_SCAN_SHAPE");
+  int fG = 0, fW = 0;
+  if (force) sscanf(force, "%d,%d", &fG, &fW);
+  for (const auto& sh0 : shapes) {
+    auto sh = sh0;
+    if (fG) {
+      if (&sh0 != &shapes[0]) break;
+      sh.G = fG;
+      sh.warps = fW;
+      sh.tsmem = true;
+    }
+    const size_t groups = (count + sh.G - 1) / sh.G;
+    const long long U = (long long)groups * t.n;
+    const long long seg = (U + ctas - 1) / ctas;  // clients one lane counter can see (upper bound)
     for (int pass = 0; pass < 2; ++pass) {
-      const int blocks_per_sm = 1;
-      const int ctas = sms * blocks_per_sm;
-      const long long U = (long long)groups * t.n;
-      const long long seg = (U + ctas - 1) / ctas;  // clients one lane-counter can see
-      const unsigned long long vmax =
-          depth_mode ? (unsigned long long)t.Wp : (unsigned long long)t.max_cost;
       const bool acc32 =
           pass == 0 && (unsigned long long)std::min<long long>(seg, t.n) * vmax < (1ull << 32);
       if (pass == 0 && !acc32) continue;
-      const size_t smem = scan_smem(t.m, warps, acc32, tsmem);
-      if (smem <= max_smem) {
-        sp.tsmem = tsmem;
-        sp.warps = warps;
+      const size_t smem = scan_smem(t.m, sh.warps, acc32, sh.tsmem, sh.G);
+      const size_t inflight = (size_t)sh.warps * 32 * 2 * chunk_bytes;  // L1 room for prefetches
+      if (smem <= max_smem && (fG || !sh.tsmem || smem + inflight <= l1_total)) {
+        sp.G = sh.G;
+        sp.tsmem = sh.tsmem;
+        sp.warps = sh.warps;
         sp.acc32 = acc32;
         sp.smem = smem;
         sp.ctas = ctas;
@@ -285,25 +382,25 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
       }
     }
   }
-  sp.ctas = 0;  // does not fit: caller must use the gather kernel
+  sp.ctas = 0;
   return sp;
 }
 
 cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* T, size_t count,
                         unsigned long long* costs_acc, unsigned long long* err_first_bad,
                         int depth_mode, cudaStream_t st) {
-  const void* fn = scan_kernel_ptr(t, sp.acc32, sp.tsmem);
+  g_depth = depth_mode != 0;
+  const void* fn = scan_kernel_ptr(t, sp.acc32, sp.G, sp.tsmem);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem);
   if (e != cudaSuccess) return e;
-  const int groups = (int)((count + 63) / 64);
-  const int ctas = std::min<long long>(sp.ctas, (long long)groups * t.n);
+  const int groups = (int)((count + sp.G - 1) / sp.G);
+  const int ctas = (int)std::min<long long>(sp.ctas, (long long)groups * t.n);
   size_t Ts = scan_t_stride(t.m);
   const void* ord = t.ord;
   const void* dist = t.dist;
   int n = t.n, Wp = t.Wp;
   void* args[] = {(void*)&ord, (void*)&dist, (void*)&n, (void*)&Wp, (void*)&T, (void*)&Ts,
-                  (void*)&count, (void*)&groups, (void*)&costs_acc, (void*)&err_first_bad,
-                  (void*)&depth_mode};
+                  (void*)&count, (void*)&groups, (void*)&costs_acc, (void*)&err_first_bad};
   e = cudaLaunchKernel(fn, dim3(ctas), dim3(sp.warps * 32), args, sp.smem, st);
   return e != cudaSuccess ? e : cudaGetLastError();
 }

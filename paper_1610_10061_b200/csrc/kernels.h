@@ -22,7 +22,7 @@ struct BuildPlan {
 };
 
 size_t sort_smem_header();
-cudaError_t launch_scan_costs(const int64_t* costs, size_t count, unsigned long long* out_max,
+cudaError_t launch_validate_costs(const int64_t* costs, size_t count, unsigned long long* out_max,
                               int* out_neg, int sms, cudaStream_t st);
 cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
                               void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st);
@@ -51,6 +51,7 @@ struct ScanPlan {
   int ctas = 0;
   bool acc32 = true;
   bool tsmem = true;  // masks staged in shared memory (else read from global)
+  int G = 64;         // chromosomes per group (64 or 32)
   size_t smem = 0;
 };
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode);

@@ -31,7 +31,7 @@ namespace pmb {
 
 // ---- validation scan: max cost and negativity (instance.cpp:20-24) --------
 
-__global__ void k_scan_costs(const int64_t* __restrict__ costs, size_t count,
+__global__ void k_validate_costs(const int64_t* __restrict__ costs, size_t count,
                              unsigned long long* __restrict__ out_max, int* __restrict__ out_neg) {
   int64_t mx = 0;
   int neg = 0;
@@ -249,10 +249,10 @@ __global__ void k_transpose_costs(const int64_t* __restrict__ costs, int n, int 
 
 // ---- host launchers --------------------------------------------------------
 
-cudaError_t launch_scan_costs(const int64_t* costs, size_t count, unsigned long long* out_max,
+cudaError_t launch_validate_costs(const int64_t* costs, size_t count, unsigned long long* out_max,
                               int* out_neg, int sms, cudaStream_t st) {
   const int blocks = (int)std::min<size_t>((size_t)sms * 8, (count + 255) / 256 + 1);
-  k_scan_costs<<<blocks, 256, 0, st>>>(costs, count, out_max, out_neg);
+  k_validate_costs<<<blocks, 256, 0, st>>>(costs, count, out_max, out_neg);
   return cudaGetLastError();
 }
 
