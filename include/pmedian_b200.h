@@ -133,6 +133,69 @@ int pm_set_profiling(pm_ctx* ctx, int enabled);
  * launches since the last read, and resets. */
 int pm_profile_read(pm_ctx* ctx, double* kernel_ms, uint64_t* kernel_launches);
 
+/* ---- genetic algorithm (K3 evolve, K4 islands) ------------------------------ */
+
+enum { PM_MIGRATE_BLOCK = 0, PM_MIGRATE_TEAM = 1 }; /* MigrationMode, ga.hpp:22 */
+enum {
+  /* the reference's exact draw: one host stream derive(seed, {1}), BigInt
+   * unranking of a uniform rank (combinatorics.cpp:54-75, ga.cpp:226-235) --
+   * run_ga results equal the reference's bit for bit */
+  PM_POPULATION_REFERENCE = 0,
+  /* device draw: Floyd's algorithm per chromosome from derive(seed, {4,
+   * generation, global index}); same distribution, not the same sequence */
+  PM_POPULATION_DEVICE = 1
+};
+
+/* GaConfig (ga.hpp:24-38).  crossover_iters / mutation_iters < 0 mean "lg(nt)". */
+typedef struct pm_ga_config {
+  size_t nb;
+  size_t nt;
+  size_t evolve_limit;
+  size_t saturation;
+  uint64_t seed;
+  long long crossover_iters;
+  long long mutation_iters;
+  int migration;
+  int population;
+} pm_ga_config;
+
+/* RunResult (ga.hpp:49-56) plus work counters. */
+typedef struct pm_run_result {
+  int64_t best_cost;
+  size_t kernels_executed;
+  size_t kernel_of_best; /* 1-based */
+  double wall_time_s;
+  double evolve_time_s;        /* host time spent in the generation loop */
+  uint64_t evaluations;        /* fitness calls the reference run would make (this island) */
+  uint64_t device_evaluations; /* chromosomes evaluated on the device (includes skipped attempts) */
+} pm_run_result;
+
+/* Replaces pmedian::evolve_block (ga.hpp:100-102) for nb consecutive blocks at
+ * once: blocks = nb x cfg->nt chromosomes (host, words_per words each, block
+ * major), evolved in place with kernel index `kernel_index` and block indices
+ * first_block .. first_block+nb-1; best_cost/best_thread (nb entries) receive
+ * each block's BlockResult (the best chromosome is blocks[b][best_thread]).
+ * Every chromosome must open exactly p sites (PM_DOMAIN otherwise) -- the GA
+ * invariant; the reference only fails later, inside crossover or fitness. */
+int pm_evolve_blocks(pm_ctx* ctx, uint64_t* blocks, size_t nb, size_t words_per, const pm_ga_config* cfg,
+                     uint64_t kernel_index, size_t first_block, int64_t* best_cost, size_t* best_thread);
+
+/* Replaces pmedian::run_ga (ga.hpp:109) on the context's instance.  best_words
+ * (ceil(m/64) words) receives RunResult::best, per_kernel_best (evolve_limit
+ * entries) RunResult::per_kernel_best_costs. */
+int pm_run_ga(pm_ctx* ctx, const pm_ga_config* cfg, uint64_t* best_words, int64_t* per_kernel_best,
+              pm_run_result* result);
+
+/* Islands over processes/GPUs: this rank evolves blocks
+ * [rank*nb/world, (rank+1)*nb/world) (nb must divide evenly) and every
+ * generation exchanges its block bests through `allgather` (send `bytes`,
+ * receive world*bytes in rank order; return 0 on success), so every rank
+ * computes the same global best, stop decision and RunResult.  RNG keys use
+ * global block indices: any world size gives the identical RunResult. */
+typedef int (*pm_allgather_fn)(const void* send, size_t bytes, void* recv, void* user);
+int pm_run_ga_islands(pm_ctx* ctx, const pm_ga_config* cfg, int rank, int world, pm_allgather_fn allgather,
+                      void* user, uint64_t* best_words, int64_t* per_kernel_best, pm_run_result* result);
+
 #ifdef __cplusplus
 }
 #endif

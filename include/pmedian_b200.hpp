@@ -1,0 +1,137 @@
+// pmedian_b200.hpp -- header-only C++ view of the C ABI (include/pmedian_b200.h)
+// that keeps the reference's C++ vocabulary: pmedian::StructuralError /
+// ContractError / DomainError / BudgetError (proj/include/pmedian/errors.hpp:8-25)
+// are thrown with the reference's message texts, and the entry points carry the
+// reference names -- build_ordering (ordering.hpp:33), fitness (ordering.hpp:39),
+// min_cost_sum (instance.hpp:39) -- plus the batched evaluate_population that
+// replaces the per-chromosome loops of evolve_block (ga.cpp:147,166,183).
+//
+// Chromosomes travel as their raw words (chromosome.hpp:24,43), so a caller
+// holding pmedian::Chromosome objects passes c.words() (the one accessor the
+// reference lacks).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pmedian_b200.h"
+
+namespace pmedian {
+
+#ifndef PMEDIAN_ERRORS_DEFINED
+#define PMEDIAN_ERRORS_DEFINED
+struct StructuralError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ContractError : std::logic_error {
+  using std::logic_error::logic_error;
+};
+struct DomainError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct BudgetError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+#endif
+
+namespace b200 {
+
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// A batch failure also names the lowest failing chromosome.
+struct BatchContractError : ContractError {
+  BatchContractError(const std::string& msg, std::size_t first) : ContractError(msg), first_bad(first) {}
+  std::size_t first_bad;
+};
+
+inline void throw_status(int rc, const char* msg, std::size_t first_bad = 0) {
+  switch (rc) {
+    case PM_OK:
+      return;
+    case PM_STRUCTURAL:
+      throw StructuralError(msg);
+    case PM_CONTRACT:
+      throw BatchContractError(msg, first_bad);
+    case PM_DOMAIN:
+      throw DomainError(msg);
+    case PM_BUDGET:
+      throw BudgetError(msg);
+    default:
+      throw DeviceError(msg);
+  }
+}
+
+// Owns one pm_ctx: one device, one stream, the resident ordering tables.
+class Tables {
+ public:
+  explicit Tables(int device = 0) {
+    const int rc = pm_create(device, &ctx_);
+    if (rc != PM_OK) throw_status(rc, "pm_create failed");
+  }
+  Tables(const Tables&) = delete;
+  Tables& operator=(const Tables&) = delete;
+  Tables(Tables&& o) noexcept : ctx_(std::exchange(o.ctx_, nullptr)) {}
+  ~Tables() { pm_destroy(ctx_); }
+
+  pm_ctx* handle() const { return ctx_; }
+
+  // Instance validation + build_ordering on the device (instance.cpp:10-30, ordering.cpp:10-38).
+  void build(const std::vector<std::int64_t>& costs, std::size_t n, std::size_t m, std::size_t p) {
+    if (costs.size() != n * m) throw StructuralError("cost matrix must be exactly n rows by m columns");
+    check(pm_set_instance(ctx_, costs.data(), n, m, p));
+  }
+
+  pm_table_info info() const {
+    pm_table_info ti{};
+    check(pm_table_info_get(ctx_, &ti));
+    return ti;
+  }
+
+  // The reference layout (OrderingTables::site_order / ::increments, ordering.hpp:22-23).
+  void copy_tables(std::vector<std::uint32_t>& site_order, std::vector<std::int64_t>& increments) const {
+    const pm_table_info ti = info();
+    site_order.resize(ti.clients * ti.width);
+    increments.resize(ti.clients * ti.width);
+    check(pm_get_tables(ctx_, site_order.data(), increments.data()));
+  }
+
+  // One fitness() per chromosome, bit-identical to ordering.cpp:40-59.
+  std::vector<std::int64_t> evaluate_population(const std::vector<std::uint64_t>& words,
+                                                std::size_t count) const {
+    std::vector<std::int64_t> out(count);
+    if (count == 0) return out;
+    const std::size_t wp = words.size() / count;
+    std::size_t bad = 0;
+    const int rc = pm_evaluate(ctx_, words.data(), count, wp, out.data(), &bad);
+    if (rc != PM_OK) throw_status(rc, pm_last_error(ctx_), bad);
+    return out;
+  }
+
+  std::int64_t fitness(const std::vector<std::uint64_t>& words) const {
+    return evaluate_population(words, 1)[0];
+  }
+
+  std::vector<std::int64_t> min_cost_sum(const std::vector<std::uint64_t>& words, std::size_t count) const {
+    std::vector<std::int64_t> out(count);
+    if (count == 0) return out;
+    std::size_t bad = 0;
+    const int rc = pm_min_cost_sum(ctx_, words.data(), count, words.size() / count, out.data(), &bad);
+    if (rc != PM_OK) throw_status(rc, pm_last_error(ctx_), bad);
+    return out;
+  }
+
+ private:
+  void check(int rc) const {
+    if (rc != PM_OK) throw_status(rc, pm_last_error(ctx_));
+  }
+  pm_ctx* ctx_ = nullptr;
+};
+
+}  // namespace b200
+}  // namespace pmedian

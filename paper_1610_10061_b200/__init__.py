@@ -50,6 +50,28 @@ _lib.pm_set_profiling.argtypes = [_vp, C.c_int]
 _lib.pm_profile_read.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
 
 
+class GaConfig(C.Structure):
+    """pmedian::GaConfig (ga.hpp:24-38); crossover/mutation_iters < 0 mean lg(nt)."""
+    _fields_ = [("nb", _sz), ("nt", _sz), ("evolve_limit", _sz), ("saturation", _sz),
+                ("seed", C.c_uint64), ("crossover_iters", C.c_longlong),
+                ("mutation_iters", C.c_longlong), ("migration", C.c_int), ("population", C.c_int)]
+
+
+class _RunResult(C.Structure):
+    _fields_ = [("best_cost", C.c_int64), ("kernels_executed", _sz), ("kernel_of_best", _sz),
+                ("wall_time_s", C.c_double), ("evolve_time_s", C.c_double),
+                ("evaluations", C.c_uint64), ("device_evaluations", C.c_uint64)]
+
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_lib.pm_evolve_blocks.argtypes = [_vp, _vp, _sz, _sz, C.POINTER(GaConfig), C.c_uint64, _sz, _vp, _vp]
+_lib.pm_run_ga.argtypes = [_vp, C.POINTER(GaConfig), _vp, _vp, C.POINTER(_RunResult)]
+_lib.pm_run_ga_islands.argtypes = [_vp, C.POINTER(GaConfig), C.c_int, C.c_int, ALLGATHER_FN, _vp, _vp,
+                                   _vp, C.POINTER(_RunResult)]
+MIGRATE_BLOCK, MIGRATE_TEAM = 0, 1
+POPULATION_REFERENCE, POPULATION_DEVICE = 0, 1
+
+
 class _TableInfo(C.Structure):
     _fields_ = [("clients", _sz), ("sites", _sz), ("open_count", _sz), ("width", _sz),
                 ("row_stride", _sz), ("site_bytes", C.c_int), ("dist_bytes", C.c_int),
@@ -64,8 +86,41 @@ C_ABI_SYMBOLS = (
     "pm_set_instance", "pm_set_instance_device", "pm_table_info_get", "pm_get_tables",
     "pm_evaluate", "pm_evaluate_device", "pm_check_errors", "pm_set_eval_kernel",
     "pm_auto_eval_kernel", "pm_min_cost_sum", "pm_scan_depths_device", "pm_set_profiling",
-    "pm_profile_read",
+    "pm_profile_read", "pm_evolve_blocks", "pm_run_ga", "pm_run_ga_islands",
 )
+
+
+def ga_config(nb=60, nt=256, evolve_limit=100, saturation=10, seed=1, crossover_iters=None,
+              mutation_iters=None, team=False, population="reference") -> GaConfig:
+    return GaConfig(nb, nt, evolve_limit, saturation, seed,
+                    -1 if crossover_iters is None else crossover_iters,
+                    -1 if mutation_iters is None else mutation_iters,
+                    MIGRATE_TEAM if team else MIGRATE_BLOCK,
+                    POPULATION_REFERENCE if population == "reference" else POPULATION_DEVICE)
+
+
+def torch_allgather(group=None, device=None):
+    """An island allgather over torch.distributed (gloo on CPU tensors, NCCL on
+    CUDA tensors) in the pm_allgather_fn shape."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(send, nbytes, recv, _user):
+        try:
+            world = dist.get_world_size(group)
+            src = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), shape=(nbytes,))
+            t = torch.from_numpy(src.copy())
+            if device is not None:
+                t = t.to(device)
+            outs = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(outs, t, group=group)
+            dst = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)), shape=(nbytes * world,))
+            dst[:] = torch.cat(outs).cpu().numpy()
+            return 0
+        except Exception:
+            return 1
+
+    return fn
 
 
 # ---- errors: pmedian/errors.hpp:8-25 --------------------------------------------
@@ -250,6 +305,38 @@ class Context:
         ms, n = C.c_double(0), C.c_uint64(0)
         self._check(_lib.pm_profile_read(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    # ---- GA (ga.cpp) ----------------------------------------------------------------
+    def evolve_blocks(self, blocks, cfg: GaConfig, kernel_index: int, first_block: int = 0):
+        """pmedian::evolve_block over nb = len(blocks)/cfg.nt consecutive blocks (in place on a
+        copy).  -> (blocks_out [nb*nt, wp], best_cost[nb], best_thread[nb])"""
+        b = np.ascontiguousarray(blocks, dtype=np.uint64).copy()
+        if b.ndim == 1:
+            b = b[None, :]
+        nb = b.shape[0] // cfg.nt
+        bc = np.zeros(max(nb, 1), dtype=np.int64)
+        bt = np.zeros(max(nb, 1), dtype=np.uint64)
+        self._check(_lib.pm_evolve_blocks(self._h, b.ctypes.data, nb, b.shape[1], C.byref(cfg), kernel_index,
+                                          first_block, bc.ctypes.data, bt.ctypes.data))
+        return b, bc[:nb], bt[:nb].astype(np.int64)
+
+    def run_ga(self, cfg: GaConfig, rank: int = 0, world: int = 1, allgather=None):
+        """pmedian::run_ga -> dict with the RunResult fields (ga.hpp:49-56) and work counters."""
+        wp = words_per(self.m)
+        best = np.zeros(wp, dtype=np.uint64)
+        per = np.zeros(cfg.evolve_limit, dtype=np.int64)
+        r = _RunResult()
+        if world == 1 and allgather is None:
+            rc = _lib.pm_run_ga(self._h, C.byref(cfg), best.ctypes.data, per.ctypes.data, C.byref(r))
+        else:
+            cb = ALLGATHER_FN(allgather)
+            rc = _lib.pm_run_ga_islands(self._h, C.byref(cfg), rank, world, cb, None, best.ctypes.data,
+                                        per.ctypes.data, C.byref(r))
+        self._check(rc)
+        return dict(best=best, best_cost=r.best_cost, kernels_executed=r.kernels_executed,
+                    kernel_of_best=r.kernel_of_best, per_kernel_best_costs=per[:r.kernels_executed].copy(),
+                    wall_time=r.wall_time_s, evolve_time=r.evolve_time_s, evaluations=r.evaluations,
+                    device_evaluations=r.device_evaluations)
 
     def min_cost_sum(self, words: np.ndarray) -> np.ndarray:
         """instance.cpp:32-48 per chromosome (gather-min, no scan-width contract)."""

@@ -12,91 +12,9 @@
 
 #include "../../include/pmedian_b200.h"
 #include "kernels.h"
+#include "ctx.h"
 
 using namespace pmb;
-
-namespace {
-
-// Reference message texts (errors thrown by the code each status replaces).
-constexpr const char* kMsgLength = "chromosome length must equal the site count";  // ordering.cpp:42
-constexpr const char* kMsgRunoff =
-    "no open site within the scan width; exactly p sites must be open";  // ordering.cpp:51
-constexpr const char* kMsgNoneOpen = "at least one site must be open";  // instance.cpp:37
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  cudaError_t ensure(size_t want) {
-    if (want <= bytes) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) bytes = want;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
-
-}  // namespace
-
-struct pm_ctx {
-  int device = 0;
-  int sms = 148;
-  size_t max_smem = 0;
-  cudaStream_t own = nullptr;
-  cudaStream_t stream = nullptr;
-  std::string err;
-  uint64_t launches = 0;
-  int eval_kind = PM_EVAL_AUTO;
-
-  bool has_instance = false;
-  DevTables t;
-  BuildPlan plan;
-  DevBuf ord, dist, dT;
-
-  // scratch
-  DevBuf costs_in, sort_keys, sort_pay, words, costs_out, T, lists, counts, errw, scal;
-  int open_cap = 0;
-
-  // kernel timing hook: events around the dominant evaluation kernel
-  bool profiling = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
-  std::pair<cudaEvent_t, cudaEvent_t> ev_get() {
-    if (!ev_free.empty()) {
-      auto e = ev_free.back();
-      ev_free.pop_back();
-      return e;
-    }
-    std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
-    cudaEventCreate(&e.first);
-    cudaEventCreate(&e.second);
-    return e;
-  }
-
-  int fail(int code, const std::string& msg) {
-    err = msg;
-    return code;
-  }
-  int cuda_fail(cudaError_t e, const char* where) {
-    err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
-    return PM_CUDA;
-  }
-};
-
-#define PM_CUDA_TRY(ctx, expr)                              \
-  do {                                                      \
-    cudaError_t _e = (expr);                                \
-    if (_e != cudaSuccess) return (ctx)->cuda_fail(_e, #expr); \
-  } while (0)
 
 extern "C" {
 
@@ -333,7 +251,10 @@ int pm_auto_eval_kernel(pm_ctx* c) {
 
 // mode: 0 fitness (ordering.cpp:40-59), 1 min_cost_sum (instance.cpp:32-48),
 // 2 scan depths (sum_i k*_i, the roofline's work measure).
-static int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcosts, int mode) {
+}  // extern "C"
+
+namespace pmb {
+int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcosts, int mode) {
   const DevTables& t = c->t;
   const int wp = (t.m + 63) / 64;
   PM_CUDA_TRY(c, cudaMemsetAsync(dcosts, 0, count * 8, c->stream));
@@ -375,6 +296,10 @@ static int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_
   c->launches += 2;
   return PM_OK;
 }
+
+}  // namespace pmb
+
+extern "C" {
 
 int pm_check_errors(pm_ctx* c, size_t* first_bad) {
   if (!c) return PM_STRUCTURAL;

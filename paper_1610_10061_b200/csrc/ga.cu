@@ -1,0 +1,538 @@
+// K3: the GA's evolve_block on the device, batched over every block, plus the
+// run_ga generation loop (K4 islands: blocks sharded over processes/GPUs,
+// one allgather of block bests per generation).
+//
+// Reference semantics (proj/src/ga.cpp) reproduced exactly:
+//  * evolve_block (:136-194): fitness of the block; `rounds` crossover rounds
+//    over the snapshot `before`, couples t ^ (nt >> (round % lg nt + 1)),
+//    both partners drawing (start, exchanges) from derive(seed, {2, kernel,
+//    block, round, min(t, couple)}); strict-improvement replacement; then
+//    `attempts` shift mutations per thread from derive(seed, {3, kernel, block,
+//    t}) stopping at the first strict improvement; min-reduce, ties to the
+//    lower thread.
+//  * run_ga (:219-303): per generation evolve all blocks, draw the next
+//    population, global best by strict < (lowest block wins ties), stale
+//    counter, stop rule, migration only when continuing.
+// The mutation attempts of a thread all mutate the same parent (the parent
+// only changes on success, and success ends the attempts), and the RNG stream
+// advances identically whether or not an attempt succeeds -- so all attempts
+// are generated and evaluated as one batch and the first improving one is
+// taken.  This evaluates attempts the reference would skip; they are counted
+// separately (device_evaluations) and never reported as reference work.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "combinatorics.h"
+#include "ctx.h"
+#include "ga_ops.cuh"
+
+namespace pmb {
+
+// ---- kernels ----------------------------------------------------------------------
+
+__global__ void k_crossover_children(const uint64_t* __restrict__ before, uint64_t* __restrict__ child,
+                                     uint8_t* __restrict__ ok, int nbl, int nt, int wp, int m, int p,
+                                     uint64_t seed, uint64_t kernel, uint64_t block0, uint64_t round,
+                                     int cycle) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nbl * nt) return;
+  const int b = idx / nt, t = idx % nt;
+  const uint32_t couple = crossover_couple((uint32_t)t, (uint32_t)(round % cycle), (uint32_t)nt);
+  const uint64_t key[5] = {kCoupleTag, kernel, block0 + b, round, (uint64_t)min((uint32_t)t, couple)};
+  Stream rng = Stream::derive(seed, key, 5);
+  const int start = (int)rng.below((uint64_t)m);
+  const int exchanges = 2 * (1 + (int)rng.below((uint64_t)(p / 2)));
+  const uint64_t* a = before + (size_t)idx * wp;
+  const uint64_t* bb = before + ((size_t)b * nt + couple) * wp;
+  uint64_t* c = child + (size_t)idx * wp;
+  const bool success = crossover(a, bb, c, m, start, exchanges);
+  if (!success)  // keep the parent (ga.cpp:165)
+    for (int w = 0; w < wp; ++w) c[w] = a[w];
+  ok[idx] = success;
+}
+
+__global__ void k_crossover_accept(uint64_t* __restrict__ pop, int64_t* __restrict__ cost,
+                                   const uint64_t* __restrict__ child, const int64_t* __restrict__ ccost,
+                                   const uint8_t* __restrict__ ok, int count, int wp,
+                                   unsigned long long* __restrict__ evals) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long e = 0;
+  if (idx < count && ok[idx]) {
+    e = 1;  // the reference evaluates every successful child (ga.cpp:166)
+    if (ccost[idx] < cost[idx]) {
+      for (int w = 0; w < wp; ++w) pop[(size_t)idx * wp + w] = child[(size_t)idx * wp + w];
+      cost[idx] = ccost[idx];
+    }
+  }
+  e = __reduce_add_sync(0xffffffffu, (unsigned)e);
+  if ((threadIdx.x & 31) == 0 && e) atomicAdd(evals, e);
+}
+
+__global__ void k_mutation_children(const uint64_t* __restrict__ pop, uint64_t* __restrict__ child,
+                                    int nbl, int nt, int wp, int m, uint64_t seed, uint64_t kernel,
+                                    uint64_t block0, int attempts) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nbl * nt) return;
+  const int b = idx / nt, t = idx % nt;
+  const uint64_t key[4] = {kMutationTag, kernel, block0 + b, (uint64_t)t};
+  Stream rng = Stream::derive(seed, key, 4);
+  const uint64_t* parent = pop + (size_t)idx * wp;
+  for (int a = 0; a < attempts; ++a)
+    random_shift_mutation(parent, child + ((size_t)idx * attempts + a) * wp, m, rng);
+}
+
+__global__ void k_mutation_accept(uint64_t* __restrict__ pop, int64_t* __restrict__ cost,
+                                  const uint64_t* __restrict__ child, const int64_t* __restrict__ ccost,
+                                  int count, int attempts, int wp, unsigned long long* __restrict__ evals) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned e = 0;
+  if (idx < count) {
+    e = attempts;
+    for (int a = 0; a < attempts; ++a) {
+      const size_t ci = (size_t)idx * attempts + a;
+      if (ccost[ci] < cost[idx]) {  // first strict improvement wins (ga.cpp:184-187)
+        for (int w = 0; w < wp; ++w) pop[(size_t)idx * wp + w] = child[ci * wp + w];
+        cost[idx] = ccost[ci];
+        e = a + 1;
+        break;
+      }
+    }
+  }
+  e = __reduce_add_sync(0xffffffffu, e);
+  if ((threadIdx.x & 31) == 0 && e) atomicAdd(evals, (unsigned long long)e);
+}
+
+// block_min_reduce (ga.cpp:113-134): lexicographic (cost, thread) minimum.
+__global__ void k_block_min(const int64_t* __restrict__ cost, const uint64_t* __restrict__ pop, int nt,
+                            int wp, int64_t* __restrict__ bcost, uint64_t* __restrict__ bthread,
+                            uint64_t* __restrict__ bwords) {
+  __shared__ int64_t sc[32];
+  __shared__ int st[32];
+  const int b = blockIdx.x;
+  int64_t best = INT64_MAX;
+  int bt = INT32_MAX;
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    const int64_t c = cost[(size_t)b * nt + t];
+    if (c < best || (c == best && t < bt)) {
+      best = c;
+      bt = t;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t c = __shfl_xor_sync(0xffffffffu, best, o);
+    const int t = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (c < best || (c == best && t < bt)) {
+      best = c;
+      bt = t;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sc[warp] = best;
+    st[warp] = bt;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    best = lane < nw ? sc[lane] : INT64_MAX;
+    bt = lane < nw ? st[lane] : INT32_MAX;
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t c = __shfl_xor_sync(0xffffffffu, best, o);
+      const int t = __shfl_xor_sync(0xffffffffu, bt, o);
+      if (c < best || (c == best && t < bt)) {
+        best = c;
+        bt = t;
+      }
+    }
+    if (lane == 0) {
+      sc[0] = best;
+      st[0] = bt;
+      bcost[b] = best;
+      bthread[b] = (uint64_t)bt;
+    }
+  }
+  __syncthreads();
+  const int t = st[0];
+  for (int w = threadIdx.x; w < wp; w += blockDim.x) bwords[(size_t)b * wp + w] = pop[((size_t)b * nt + t) * wp + w];
+}
+
+// Device-native population draw: uniform p-subsets by Floyd's algorithm from a
+// keyed splitmix stream derive(seed, {4, generation, global chromosome}).
+// (Not the reference's BigInt unranking -- see population mode in pmedian_b200.h.)
+__global__ void k_draw_population(uint64_t* __restrict__ pop, int count, int wp, int m, int p,
+                                  uint64_t seed, uint64_t generation, uint64_t index0) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  uint64_t* w = pop + (size_t)idx * wp;
+  for (int i = 0; i < wp; ++i) w[i] = 0;
+  const uint64_t key[3] = {4, generation, index0 + idx};
+  Stream rng = Stream::derive(seed, key, 3);
+  for (int j = m - p; j < m; ++j) {
+    const int r = (int)rng.below((uint64_t)j + 1);
+    const uint64_t bit = 1ull << (r & 63);
+    if (w[r >> 6] & bit) w[j >> 6] |= 1ull << (j & 63);
+    else w[r >> 6] |= bit;
+  }
+}
+
+__global__ void k_popcount_check(const uint64_t* __restrict__ pop, int count, int wp, int m, int p,
+                                 unsigned long long* __restrict__ bad) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  int pc = 0;
+  for (int w = 0; w < wp; ++w) {
+    uint64_t x = pop[(size_t)idx * wp + w];
+    if (w == wp - 1 && (m & 63)) x &= (1ull << (m & 63)) - 1;
+    pc += __popcll(x);
+  }
+  if (pc != p) atomicMin(bad, (unsigned long long)idx);
+}
+
+static unsigned cdiv(size_t a, unsigned b) { return (unsigned)((a + b - 1) / b); }
+
+// ---- GA engine ---------------------------------------------------------------------
+
+struct GaBuffers {
+  DevBuf pop, next, cost, before, child, ccost, ok, bcost, bthread, bwords, evals, tmp;
+};
+
+struct GaShape {
+  int nbl = 0, nt = 0, wp = 0, m = 0, p = 0, rounds = 0, attempts = 0, cycle = 0;
+  uint64_t seed = 0;
+  size_t block0 = 0;
+};
+
+static int lg2(size_t v) {
+  int r = 0;
+  while ((size_t{1} << r) < v) ++r;
+  return r;
+}
+
+// One evolve_block over every local block (kernel index `kernel`).
+static int evolve_all(pm_ctx* c, GaBuffers& B, const GaShape& s, uint64_t kernel) {
+  const size_t count = (size_t)s.nbl * s.nt;
+  const unsigned tb = 256;
+  uint64_t* pop = B.pop.as<uint64_t>();
+  int64_t* cost = B.cost.as<int64_t>();
+  unsigned long long* evals = B.evals.as<unsigned long long>();
+  int rc = evaluate_core(c, pop, count, cost, 0);  // ga.cpp:146-147
+  if (rc) return rc;
+  if (s.p >= 2) {  // ga.cpp:154
+    for (int r = 0; r < s.rounds; ++r) {
+      PM_CUDA_TRY(c, cudaMemcpyAsync(B.before.p, pop, count * s.wp * 8, cudaMemcpyDeviceToDevice, c->stream));
+      k_crossover_children<<<cdiv(count, tb), tb, 0, c->stream>>>(
+          B.before.as<uint64_t>(), B.child.as<uint64_t>(), B.ok.as<uint8_t>(), s.nbl, s.nt, s.wp, s.m, s.p,
+          s.seed, kernel, s.block0, (uint64_t)r, s.cycle);
+      PM_CUDA_TRY(c, cudaGetLastError());
+      rc = evaluate_core(c, B.child.as<uint64_t>(), count, B.ccost.as<int64_t>(), 0);
+      if (rc) return rc;
+      k_crossover_accept<<<cdiv(count, tb), tb, 0, c->stream>>>(pop, cost, B.child.as<uint64_t>(),
+                                                                 B.ccost.as<int64_t>(), B.ok.as<uint8_t>(),
+                                                                 (int)count, s.wp, evals);
+      PM_CUDA_TRY(c, cudaGetLastError());
+      c->launches += 2;
+    }
+  }
+  if (s.attempts > 0) {
+    k_mutation_children<<<cdiv(count, tb), tb, 0, c->stream>>>(pop, B.child.as<uint64_t>(), s.nbl, s.nt,
+                                                                s.wp, s.m, s.seed, kernel, s.block0,
+                                                                s.attempts);
+    PM_CUDA_TRY(c, cudaGetLastError());
+    rc = evaluate_core(c, B.child.as<uint64_t>(), count * s.attempts, B.ccost.as<int64_t>(), 0);
+    if (rc) return rc;
+    k_mutation_accept<<<cdiv(count, tb), tb, 0, c->stream>>>(pop, cost, B.child.as<uint64_t>(),
+                                                              B.ccost.as<int64_t>(), (int)count, s.attempts,
+                                                              s.wp, evals);
+    PM_CUDA_TRY(c, cudaGetLastError());
+    c->launches += 2;
+  }
+  k_block_min<<<s.nbl, 256, 0, c->stream>>>(cost, pop, s.nt, s.wp, B.bcost.as<int64_t>(),
+                                              B.bthread.as<uint64_t>(), B.bwords.as<uint64_t>());
+  PM_CUDA_TRY(c, cudaGetLastError());
+  c->launches += 1;
+  return PM_OK;
+}
+
+static int ga_alloc(pm_ctx* c, GaBuffers& B, const GaShape& s) {
+  const size_t count = (size_t)s.nbl * s.nt;
+  const size_t kids = count * std::max(1, s.attempts);
+  PM_CUDA_TRY(c, B.pop.ensure(count * s.wp * 8));
+  PM_CUDA_TRY(c, B.next.ensure(count * s.wp * 8));
+  PM_CUDA_TRY(c, B.cost.ensure(count * 8));
+  PM_CUDA_TRY(c, B.before.ensure(count * s.wp * 8));
+  PM_CUDA_TRY(c, B.child.ensure(kids * s.wp * 8));
+  PM_CUDA_TRY(c, B.ccost.ensure(kids * 8));
+  PM_CUDA_TRY(c, B.ok.ensure(count));
+  PM_CUDA_TRY(c, B.bcost.ensure((size_t)s.nbl * 8));
+  PM_CUDA_TRY(c, B.bthread.ensure((size_t)s.nbl * 8));
+  PM_CUDA_TRY(c, B.bwords.ensure((size_t)s.nbl * s.wp * 8));
+  PM_CUDA_TRY(c, B.evals.ensure(16));
+  PM_CUDA_TRY(c, B.tmp.ensure(16));
+  return PM_OK;
+}
+
+static void ga_release(GaBuffers& B) {
+  for (DevBuf* b : {&B.pop, &B.next, &B.cost, &B.before, &B.child, &B.ccost, &B.ok, &B.bcost, &B.bthread,
+                    &B.bwords, &B.evals, &B.tmp})
+    b->release();
+}
+
+// GaConfig::validate (ga.cpp:25-33), same texts.
+static int validate_config(pm_ctx* c, const pm_ga_config* cfg) {
+  if (!cfg) return c->fail(PM_STRUCTURAL, "null config");
+  if (cfg->nb < 1) return c->fail(PM_DOMAIN, "nb must be >= 1");
+  if (cfg->nt < 2 || (cfg->nt & (cfg->nt - 1)) != 0) return c->fail(PM_DOMAIN, "nt must be a power of two >= 2");
+  if (cfg->evolve_limit < 1) return c->fail(PM_DOMAIN, "evolve_limit must be >= 1");
+  if (cfg->saturation < 1) return c->fail(PM_DOMAIN, "saturation must be >= 1");
+  if (cfg->migration == PM_MIGRATE_TEAM && cfg->nb > cfg->nt) return c->fail(PM_DOMAIN, "team migration needs nb <= nt");
+  if (cfg->population != PM_POPULATION_REFERENCE && cfg->population != PM_POPULATION_DEVICE)
+    return c->fail(PM_DOMAIN, "unknown population mode");
+  return PM_OK;
+}
+
+static GaShape make_shape(pm_ctx* c, const pm_ga_config* cfg, size_t nbl, size_t block0) {
+  GaShape s;
+  s.nbl = (int)nbl;
+  s.nt = (int)cfg->nt;
+  s.m = c->t.m;
+  s.p = c->t.p;
+  s.wp = (s.m + 63) / 64;
+  s.cycle = lg2(cfg->nt);
+  s.rounds = cfg->crossover_iters >= 0 ? (int)cfg->crossover_iters : s.cycle;
+  s.attempts = cfg->mutation_iters >= 0 ? (int)cfg->mutation_iters : s.cycle;
+  s.seed = cfg->seed;
+  s.block0 = block0;
+  return s;
+}
+
+// Reference-exact population (ga.cpp:226-235): one host stream derive(seed,
+// {1}) drawing nb*nt ranks in order; this rank unranks its own blocks
+// (the draws of other ranks' blocks are consumed to stay in step).
+struct HostDraw {
+  Stream stream;
+  UBig bound;
+  size_t m = 0, p = 0;
+  void init(uint64_t seed, size_t m_, size_t p_) {
+    const uint64_t key[1] = {kHostTag};
+    stream = Stream::derive(seed, key, 1);
+    m = m_;
+    p = p_;
+    bound = binomial(m, p);
+  }
+  void draw(size_t total, size_t lo, size_t hi, uint64_t* out /* (hi-lo) x wp */) {
+    std::vector<UBig> ranks;
+    ranks.reserve(hi - lo);
+    for (size_t i = 0; i < total; ++i) {
+      UBig r = random_below(bound, stream);
+      if (i >= lo && i < hi) ranks.push_back(std::move(r));
+    }
+    const size_t wp = (m + 63) / 64, n = ranks.size();
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const unsigned workers = (unsigned)std::min<size_t>(hw, std::max<size_t>(1, n / 64));
+    auto work = [&](unsigned w) {
+      for (size_t i = n * w / workers; i < n * (w + 1) / workers; ++i) unrank_combination(m, p, ranks[i], out + i * wp);
+    };
+    if (workers <= 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (unsigned w = 0; w < workers; ++w) pool.emplace_back(work, w);
+      for (auto& th : pool) th.join();
+    }
+  }
+};
+
+}  // namespace pmb
+
+using namespace pmb;
+
+extern "C" {
+
+int pm_evolve_blocks(pm_ctx* c, uint64_t* blocks, size_t nb, size_t words_per, const pm_ga_config* cfg,
+                     uint64_t kernel_index, size_t first_block, int64_t* best_cost, size_t* best_thread) {
+  if (!c) return PM_STRUCTURAL;
+  if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
+  int rc = validate_config(c, cfg);
+  if (rc) return rc;
+  if (words_per != (size_t)(c->t.m + 63) / 64) return c->fail(PM_STRUCTURAL, kMsgLength);
+  if (nb == 0) return PM_OK;
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  GaBuffers B;
+  const GaShape s = make_shape(c, cfg, nb, first_block);
+  rc = ga_alloc(c, B, s);
+  if (rc) return rc;
+  const size_t count = nb * cfg->nt;
+  PM_CUDA_TRY(c, cudaMemcpyAsync(B.pop.p, blocks, count * s.wp * 8, cudaMemcpyHostToDevice, c->stream));
+  // every chromosome must open exactly p sites (the GA's invariant; see pmedian_b200.h)
+  unsigned long long bad = ~0ull;
+  PM_CUDA_TRY(c, cudaMemcpyAsync(B.tmp.p, &bad, 8, cudaMemcpyHostToDevice, c->stream));
+  k_popcount_check<<<cdiv(count, 256), 256, 0, c->stream>>>(B.pop.as<uint64_t>(), (int)count, s.wp, s.m, s.p,
+                                                             B.tmp.as<unsigned long long>());
+  PM_CUDA_TRY(c, cudaMemcpyAsync(&bad, B.tmp.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (bad != ~0ull) {
+    ga_release(B);
+    return c->fail(PM_DOMAIN, "every chromosome of an evolved block must open exactly p sites");
+  }
+  PM_CUDA_TRY(c, cudaMemsetAsync(c->errw.p, 0xff, 8, c->stream));
+  PM_CUDA_TRY(c, cudaMemsetAsync(B.evals.p, 0, 8, c->stream));
+  rc = evolve_all(c, B, s, kernel_index);
+  if (rc) {
+    ga_release(B);
+    return rc;
+  }
+  std::vector<int64_t> bc(nb);
+  std::vector<uint64_t> bt(nb);
+  PM_CUDA_TRY(c, cudaMemcpyAsync(blocks, B.pop.p, count * s.wp * 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(bc.data(), B.bcost.p, nb * 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(bt.data(), B.bthread.p, nb * 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  ga_release(B);
+  size_t fb = 0;
+  rc = pm_check_errors(c, &fb);
+  if (rc) return rc;
+  for (size_t b = 0; b < nb; ++b) {
+    if (best_cost) best_cost[b] = bc[b];
+    if (best_thread) best_thread[b] = (size_t)bt[b];
+  }
+  return PM_OK;
+}
+
+int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, pm_allgather_fn allgather,
+                      void* user, uint64_t* best_words, int64_t* per_kernel_best, pm_run_result* res) {
+  if (!c) return PM_STRUCTURAL;
+  if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
+  int rc = validate_config(c, cfg);
+  if (rc) return rc;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !allgather))
+    return c->fail(PM_DOMAIN, "invalid island layout");
+  if (cfg->nb % (size_t)world != 0) return c->fail(PM_DOMAIN, "nb must be a multiple of the number of islands");
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  const size_t nb = cfg->nb, nt = cfg->nt, nbl = nb / world, block0 = nbl * rank;
+  GaBuffers B;
+  const GaShape s = make_shape(c, cfg, nbl, block0);
+  rc = ga_alloc(c, B, s);
+  if (rc) return rc;
+  const size_t count = nbl * nt, wp = s.wp;
+  const bool ref_draw = cfg->population == PM_POPULATION_REFERENCE;
+  HostDraw hd;
+  std::vector<uint64_t> host_pop;
+  if (ref_draw) {
+    hd.init(cfg->seed, s.m, s.p);
+    host_pop.resize(count * wp);
+  }
+  auto draw = [&](DevBuf& dst, uint64_t generation) -> int {
+    if (ref_draw) {
+      hd.draw(nb * nt, block0 * nt, (block0 + nbl) * nt, host_pop.data());
+      PM_CUDA_TRY(c, cudaMemcpyAsync(dst.p, host_pop.data(), count * wp * 8, cudaMemcpyHostToDevice, c->stream));
+    } else {
+      k_draw_population<<<cdiv(count, 256), 256, 0, c->stream>>>(dst.as<uint64_t>(), (int)count, (int)wp, s.m,
+                                                                  s.p, cfg->seed, generation, block0 * nt);
+      PM_CUDA_TRY(c, cudaGetLastError());
+      c->launches += 1;
+    }
+    return PM_OK;
+  };
+  PM_CUDA_TRY(c, cudaMemsetAsync(c->errw.p, 0xff, 8, c->stream));
+  PM_CUDA_TRY(c, cudaMemsetAsync(B.evals.p, 0, 8, c->stream));
+  rc = draw(B.pop, 0);
+  if (rc) return rc;
+
+  // per-block record exchanged between islands: {cost, thread, words[wp]}
+  const size_t rec = 2 + wp;
+  std::vector<uint64_t> local(nbl * rec), global(nb * rec);
+  std::vector<int64_t> bc(nbl);
+  std::vector<uint64_t> bt(nbl), bw(nbl * wp);
+  int64_t best_cost = std::numeric_limits<int64_t>::max();
+  std::vector<uint64_t> best(wp, 0);
+  size_t stale = 0, kernels = 0, kernel_of_best = 0;
+  uint64_t device_evals = 0;
+  double evolve_s = 0;
+  const size_t kids_per_gen = count * (1 + (s.p >= 2 ? s.rounds : 0) + s.attempts);
+  for (uint64_t kernel = 0;; ++kernel) {
+    const auto g0 = std::chrono::steady_clock::now();
+    rc = evolve_all(c, B, s, kernel);
+    if (rc) return rc;
+    device_evals += kids_per_gen;
+    // draw the next population while the device evolves (ga.cpp:274)
+    rc = draw(B.next, kernel + 1);
+    if (rc) return rc;
+    PM_CUDA_TRY(c, cudaMemcpyAsync(bc.data(), B.bcost.p, nbl * 8, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA_TRY(c, cudaMemcpyAsync(bt.data(), B.bthread.p, nbl * 8, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA_TRY(c, cudaMemcpyAsync(bw.data(), B.bwords.p, nbl * wp * 8, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    evolve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - g0).count();
+    for (size_t b = 0; b < nbl; ++b) {
+      local[b * rec] = (uint64_t)bc[b];
+      local[b * rec + 1] = bt[b];
+      std::memcpy(&local[b * rec + 2], &bw[b * wp], wp * 8);
+    }
+    if (world > 1) {
+      if (allgather(local.data(), local.size() * 8, global.data(), user) != 0)
+        return c->fail(PM_NCCL, "island allgather failed");
+    } else {
+      global = local;
+    }
+    size_t best_block = 0;  // ga.cpp:279-282: strict <, lowest block wins ties
+    for (size_t b = 1; b < nb; ++b)
+      if ((int64_t)global[b * rec] < (int64_t)global[best_block * rec]) best_block = b;
+    const int64_t kernel_best = (int64_t)global[best_block * rec];
+    if (per_kernel_best && kernel < cfg->evolve_limit) per_kernel_best[kernel] = kernel_best;
+    if (kernel_best < best_cost) {  // ga.cpp:285-292
+      best_cost = kernel_best;
+      std::memcpy(best.data(), &global[best_block * rec + 2], wp * 8);
+      kernel_of_best = (size_t)kernel + 1;
+      stale = 0;
+    } else {
+      ++stale;
+    }
+    if (stale >= cfg->saturation || kernel + 1 >= cfg->evolve_limit) {
+      kernels = (size_t)kernel + 1;
+      break;
+    }
+    // migrate (ga.cpp:204-215) into the freshly drawn population
+    if (cfg->migration == PM_MIGRATE_BLOCK) {
+      for (size_t b = 0; b < nbl; ++b)
+        PM_CUDA_TRY(c, cudaMemcpyAsync(B.next.as<uint64_t>() + (b * nt) * wp, &global[(block0 + b) * rec + 2],
+                                       wp * 8, cudaMemcpyHostToDevice, c->stream));
+    } else if (rank == 0) {
+      for (size_t b = 0; b < nb; ++b)
+        PM_CUDA_TRY(c, cudaMemcpyAsync(B.next.as<uint64_t>() + b * wp, &global[b * rec + 2], wp * 8,
+                                       cudaMemcpyHostToDevice, c->stream));
+    }
+    std::swap(B.pop, B.next);
+  }
+  unsigned long long ref_evals = 0;
+  PM_CUDA_TRY(c, cudaMemcpyAsync(&ref_evals, B.evals.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  ga_release(B);
+  size_t fb = 0;
+  rc = pm_check_errors(c, &fb);
+  if (rc) return rc;
+  if (best_words) std::memcpy(best_words, best.data(), wp * 8);
+  if (res) {
+    res->best_cost = best_cost;
+    res->kernels_executed = kernels;
+    res->kernel_of_best = kernel_of_best;
+    res->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    res->evolve_time_s = evolve_s;
+    res->evaluations = ref_evals + (uint64_t)kernels * count;  // + the initial evaluation of each generation
+    res->device_evaluations = device_evals;
+  }
+  return PM_OK;
+}
+
+int pm_run_ga(pm_ctx* c, const pm_ga_config* cfg, uint64_t* best_words, int64_t* per_kernel_best,
+              pm_run_result* res) {
+  return pm_run_ga_islands(c, cfg, 0, 1, nullptr, nullptr, best_words, per_kernel_best, res);
+}
+
+}  // extern "C"

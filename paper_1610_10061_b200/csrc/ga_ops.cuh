@@ -1,0 +1,157 @@
+// Device restatements of the reference GA's pure building blocks:
+//   splitmix RandomStream   proj/include/pmedian/rng.hpp:11-51
+//   crossover               proj/src/ga.cpp:35-63
+//   circular/block shift    proj/src/ga.cpp:65-90
+//   random_shift_mutation   proj/src/ga.cpp:92-104
+//   crossover_couple        proj/src/ga.cpp:106-111
+// All operate on a chromosome's raw words (chromosome.hpp:24: site j = bit
+// j&63 of word j>>6) and reproduce the reference bit for bit, including every
+// RNG draw in the reference's order.  Word-level implementations: a shift
+// costs O(m/64), a crossover O(m/64 + exchange count).
+#pragma once
+
+#include <stdint.h>
+
+namespace pmb {
+
+// ---- RandomStream (rng.hpp) ---------------------------------------------------
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+struct Stream {
+  uint64_t state;
+  __host__ __device__ static Stream derive(uint64_t master, const uint64_t* key, int nkey) {
+    uint64_t s = mix64(master ^ 0x6a09e667f3bcc909ULL);
+    for (int i = 0; i < nkey; ++i) s = mix64(s ^ mix64(key[i] + 0x9e3779b97f4a7c15ULL));
+    return Stream{s};
+  }
+  __host__ __device__ uint64_t next() {
+    state += 0x9e3779b97f4a7c15ULL;
+    return mix64(state);
+  }
+  __host__ __device__ uint64_t below(uint64_t bound) {
+    if ((bound & (bound - 1)) == 0) return next() & (bound - 1);
+    const uint64_t threshold = (0 - bound) % bound;
+    uint64_t v = next();
+    while (v < threshold) v = next();
+    return v % bound;
+  }
+  __host__ __device__ bool coin() { return (next() & 1) != 0; }
+};
+
+// Key prefixes of ga.cpp:19-21.
+constexpr uint64_t kHostTag = 1, kCoupleTag = 2, kMutationTag = 3;
+
+// ---- bit helpers --------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t low_mask(int cnt) {  // cnt in [0, 64]
+  return cnt >= 64 ? ~0ull : ((1ull << cnt) - 1);
+}
+
+// cnt (<= 64) bits starting at absolute position s (no wrap).
+__device__ __forceinline__ uint64_t extract_linear(const uint64_t* w, int s, int cnt) {
+  if (cnt <= 0) return 0;
+  const int w0 = s >> 6, off = s & 63;
+  uint64_t v = w[w0] >> off;
+  if (off != 0 && off + cnt > 64) v |= w[w0 + 1] << (64 - off);
+  return v & low_mask(cnt);
+}
+
+// cnt bits of the cyclic range [base, base+len): relative positions r, r+1, ... (mod len).
+__device__ __forceinline__ uint64_t extract_cyclic(const uint64_t* w, int base, int len, int r, int cnt) {
+  if (r + cnt <= len) return extract_linear(w, base + r, cnt);
+  const int first = len - r;
+  return extract_linear(w, base + r, first) | (extract_linear(w, base, cnt - first) << first);
+}
+
+// out[lo + (t + offset) % len] = in[lo + t] for t < len; other bits copied.
+// circular_shift is the case lo = 0, len = m (ga.cpp:65-75); block_shift the
+// general one (ga.cpp:77-90).  `offset` is already reduced to [0, len).
+__device__ void rotate_range(const uint64_t* in, uint64_t* out, int m, int lo, int len, int offset) {
+  const int wp = (m + 63) >> 6;
+  const int hi = lo + len - 1;
+  for (int wi = 0; wi < wp; ++wi) {
+    uint64_t v = in[wi];
+    const int q0 = max(wi * 64, lo), q1 = min(wi * 64 + 63, hi);
+    if (q0 <= q1 && offset != 0) {
+      const int cnt = q1 - q0 + 1;
+      int r = (q0 - lo - offset) % len;
+      if (r < 0) r += len;
+      const uint64_t bits = extract_cyclic(in, lo, len, r, cnt);
+      const int sh = q0 - wi * 64;
+      const uint64_t mask = low_mask(cnt) << sh;
+      v = (v & ~mask) | ((bits << sh) & mask);
+    }
+    out[wi] = v;
+  }
+}
+
+// random_shift_mutation (ga.cpp:92-104) with the reference's draw order:
+// coin(whole), coin(direction: true = Left), then k, or a, b, k.
+__device__ void random_shift_mutation(const uint64_t* in, uint64_t* out, int m, Stream& rng) {
+  const bool whole = rng.coin();
+  const bool left = rng.coin();
+  if (whole) {
+    const int k = 1 + (int)rng.below((uint64_t)(m - 1));
+    const int offset = left ? m - k : k;  // ga.cpp:70
+    rotate_range(in, out, m, 0, m, offset % m);
+    return;
+  }
+  const int a = (int)rng.below((uint64_t)m);
+  int b = (int)rng.below((uint64_t)(m - 1));
+  if (b >= a) ++b;
+  const int lo = min(a, b), hi = max(a, b);
+  const int len = hi - lo + 1;
+  const int k = (int)rng.below((uint64_t)len);
+  const int offset = k == 0 ? 0 : (left ? len - k : k);  // ga.cpp:83-85
+  rotate_range(in, out, m, lo, len, offset);
+}
+
+// crossover (ga.cpp:35-63): child starts as a; scanning cyclically from
+// `start`, differing positions adopt b's gene while the closed->open and
+// open->closed quotas (exchanges/2 each) last.  Returns success.
+__device__ bool crossover(const uint64_t* a, const uint64_t* b, uint64_t* child, int m, int start,
+                          int exchanges) {
+  const int wp = (m + 63) >> 6;
+  for (int wi = 0; wi < wp; ++wi) child[wi] = a[wi];
+  int oq = exchanges / 2, cq = exchanges / 2;
+  // two segments: [start, m) then [0, start)
+  for (int seg = 0; seg < 2; ++seg) {
+    const int s0 = seg == 0 ? start : 0, s1 = seg == 0 ? m : start;
+    for (int wi = s0 >> 6; s0 < s1 && wi <= ((s1 - 1) >> 6); ++wi) {
+      uint64_t range = ~0ull;
+      if (wi == (s0 >> 6)) range &= ~0ull << (s0 & 63);
+      if (wi == ((s1 - 1) >> 6)) range &= low_mask(((s1 - 1) & 63) + 1);
+      const uint64_t diff = (a[wi] ^ b[wi]) & range;
+      uint64_t opn = diff & ~a[wi], cls = diff & a[wi];
+      // the position where the later quota runs out ends the scan
+      uint64_t take_o = 0, take_c = 0;
+      while (opn && oq > 0) {
+        const uint64_t lb = opn & (0 - opn);
+        take_o |= lb;
+        opn ^= lb;
+        --oq;
+      }
+      while (cls && cq > 0) {
+        const uint64_t lb = cls & (0 - cls);
+        take_c |= lb;
+        cls ^= lb;
+        --cq;
+      }
+      child[wi] = (child[wi] | take_o) & ~take_c;
+      if (oq == 0 && cq == 0) return true;
+    }
+  }
+  return false;
+}
+
+__host__ __device__ __forceinline__ uint32_t crossover_couple(uint32_t t, uint32_t round, uint32_t nt) {
+  const uint32_t sub = nt >> round, stride = sub / 2;  // ga.cpp:106-111
+  return (t % sub) >= stride ? t - stride : t + stride;
+}
+
+}  // namespace pmb

@@ -1,0 +1,95 @@
+"""Islands (K4): the run_ga block bests are exchanged with one allgather per
+generation.  CPU: the torch.distributed adapter (gloo, world_size 2) delivers
+records in rank order.  GPU: 1 vs 2 islands (two processes on one device,
+gloo exchange -- the kernels never wait on each other) give the identical
+RunResult, the reference's worker-count invariance (test_ga.cpp:401-418)."""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _allgather_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1610_10061_b200 as pm
+    fn = pm.torch_allgather()
+    send = np.arange(5, dtype=np.uint64) + 100 * rank
+    recv = np.zeros(5 * world, dtype=np.uint64)
+    rc = fn(send.ctypes.data, send.nbytes, recv.ctypes.data, None)
+    q.put((rank, rc, recv.tolist()))
+    dist.destroy_process_group()
+
+
+def test_torch_allgather_adapter_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_allgather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(60)
+    want = list(range(5)) + [100 + i for i in range(5)]
+    for rank, rc, recv in res:
+        assert rc == 0 and recv == want
+
+
+def _island_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1610_10061_b200 as pm
+    from oracle.oracle import Oracle
+    o = Oracle()
+    costs = o.synth_euclid(300)
+    ctx = pm.Context(0)
+    ctx.set_instance(costs, 300, 300, 30)
+    out = []
+    for pop in ("reference", "device"):
+        cfg = pm.ga_config(nb=8, nt=32, evolve_limit=5, saturation=5, seed=4, population=pop)
+        r = ctx.run_ga(cfg, rank=rank, world=world, allgather=pm.torch_allgather())
+        out.append((r["best_cost"], r["best"].tolist(), r["kernels_executed"], r["kernel_of_best"],
+                    r["per_kernel_best_costs"].tolist()))
+    q.put((rank, out))
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_islands_world_size_invariance():
+    import paper_1610_10061_b200 as pm
+    from oracle.oracle import Oracle
+    o = Oracle()
+    costs = o.synth_euclid(300)
+    single = []
+    with pm.Context(0) as ctx:
+        ctx.set_instance(costs, 300, 300, 30)
+        for pop in ("reference", "device"):
+            r = ctx.run_ga(pm.ga_config(nb=8, nt=32, evolve_limit=5, saturation=5, seed=4, population=pop))
+            single.append((r["best_cost"], r["best"].tolist(), r["kernels_executed"], r["kernel_of_best"],
+                           r["per_kernel_best_costs"].tolist()))
+    c = mp.get_context("spawn")
+    q = c.Queue()
+    port = _free_port()
+    procs = [c.Process(target=_island_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(60)
+    for rank, out in res:
+        assert out == single, rank

@@ -1,4 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
 exec > gpurun_out/timing.log 2>&1
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | grep -E "Error|error|assert|FAIL|passed|failed" | head -30
+timeout 1200 python -m pytest tests -x -q -m gpu -k "ga or island or cpp" 2>&1 | grep -E "Error|error|assert|FAIL|passed|failed|^E " | head -40
