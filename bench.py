@@ -76,7 +76,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -275,6 +275,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         so, inc = ctx.get_tables()
         cpu = cpu_reference_sample(so, inc, n, m, p, pop, gpu_costs, budget_s=args.cpu_seconds)
+        del so, inc
+
+    ga = None if args.no_ga else bench_ga(ctx, args, world, rank, local, n, m, p)
 
     clocks = clk.summary()
     line = {
@@ -309,6 +312,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks,
         "clocks_e2e": clk2.summary(),
+        "ga": ga,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -316,6 +320,45 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+GA_GENS = 5
+
+
+def bench_ga(ctx, args, world, rank, local, n, m, p):
+    """GA gens/s (BASELINE metric's second half).  One generation = one run_ga
+    loop iteration (ga.cpp:246-299).  Timed end to end on the host around
+    pm_run_ga (device work, host population draw, stop test, migration)."""
+    import paper_1610_10061_b200 as pm
+    from paper_1610_10061_b200 import synth
+    out = {}
+    # syn20k-shape island GA: 16 blocks x 256 per GPU, islands over the ranks
+    nb = 16 * world
+    cfg = pm.ga_config(nb=nb, nt=256, evolve_limit=GA_GENS, saturation=GA_GENS + 1, seed=1,
+                       population="device")
+    ag = None if world == 1 else pm.torch_allgather(device=f"cuda:{local}")
+    r = ctx.run_ga(cfg, rank=rank, world=world, allgather=ag)
+    out["islands"] = {"config": f"n=m={n}, p={p}, nb={nb} ({16} per GPU), nt=256, device population draw",
+                      "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
+                      "best_cost": r["best_cost"], "evals_per_gen_reference_semantics":
+                          r["evaluations"] / r["kernels_executed"],
+                      "device_evals_per_gen": r["device_evaluations"] / r["kernels_executed"]}
+    if world == 1 and rank == 0:
+        # the paper's Table-1 shape (nb=60, nt=256) on a pmed40-sized synthetic instance
+        import paper_1610_10061_b200 as pm2
+        c2 = pm2.Context(local)
+        c2.set_instance(synth.euclid_costs(900, 12345), 900, 900, 90)
+        for pop_mode in ("reference", "device"):
+            cfg = pm.ga_config(nb=60, nt=256, evolve_limit=GA_GENS, saturation=GA_GENS + 1, seed=1,
+                               population=pop_mode)
+            r = c2.run_ga(cfg)
+            out[f"pmed40_shape_{pop_mode}_population"] = {
+                "config": "synthetic Euclidean n=m=900, p=90, nb=60, nt=256 (OR-Library pmed40 absent)",
+                "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
+                "best_cost": r["best_cost"],
+                "evals_per_gen_reference_semantics": r["evaluations"] / r["kernels_executed"]}
+        c2.close()
+    return out
 
 
 def run_reference(args):
@@ -363,6 +406,16 @@ def run_reference(args):
                          "sample": f"{sample} chromosomes per step, {args.steps} steps"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    del ri
+    if not args.no_ga:
+        # the reference run_ga (ga.cpp:219-303) at the paper's Table-1 shape, all host threads
+        ri = ref.create(900, 900, 90, synth.euclid_costs(900, 12345))
+        rc, r = ri.run_ga(60, 256, 2, 10, 1, workers=threads)
+        line["ga"] = {"pmed40_shape_reference_population": {
+            "config": "synthetic Euclidean n=m=900, p=90, nb=60, nt=256; reference run_ga, "
+                      f"{threads} worker threads",
+            "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
+            "best_cost": r["best_cost"]}}
     print(json.dumps(line), flush=True)
 
 
@@ -377,6 +430,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--no-ga", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -1,4 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-exec > gpurun_out/timing.log 2>&1
-timeout 1200 python -m pytest tests -x -q -m gpu -k "ga or island or cpp" 2>&1 | grep -E "Error|error|assert|FAIL|passed|failed|^E " | head -40
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
