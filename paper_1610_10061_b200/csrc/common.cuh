@@ -24,10 +24,18 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // across CTAs through L2, not through L1).
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
+}
+
+// 32-byte variant (sm_100: LDG.E.256); p must be 32-byte aligned.
+__device__ __forceinline__ void ldg_stream32(const void* p, uint4& lo, uint4& hi) {
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z),
+                 "=r"(hi.w)
+               : "l"(p));
 }
 
 template <class T>

@@ -89,11 +89,13 @@ struct Chunk {
   uint4 o[kO];
   uint4 d[kD];
 
+  // 32-byte loads (LDG.256): one full sector per lane per instruction; rows
+  // are 32-byte aligned (Wp is a multiple of 16 elements, k of kChunk).
   __device__ __forceinline__ void load(const OrdT* orow, const DistT* drow, int k) {
 #pragma unroll
-    for (int x = 0; x < kO; ++x) o[x] = ldg_stream(reinterpret_cast<const uint4*>(orow + k) + x);
+    for (int x = 0; x < kO; x += 2) ldg_stream32(reinterpret_cast<const uint4*>(orow + k) + x, o[x], o[x + 1]);
 #pragma unroll
-    for (int x = 0; x < kD; ++x) d[x] = ldg_stream(reinterpret_cast<const uint4*>(drow + k) + x);
+    for (int x = 0; x < kD; x += 2) ldg_stream32(reinterpret_cast<const uint4*>(drow + k) + x, d[x], d[x + 1]);
   }
   __device__ __forceinline__ uint32_t site(int j) const {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(o);
@@ -166,6 +168,9 @@ __global__ void __launch_bounds__(512, 1)
   AccT* myacc = acc + (size_t)warp * kG * 32 + lane;
   MaskT* myh = hbuf + (size_t)warp * kChunk * 32 + lane;
   AccT* myd = dbuf + (size_t)warp * kChunk * 32 + lane;
+  // 32-bit mask and 32-bit cost: park both in one 8-byte slot (one STS / LDS)
+  constexpr bool kPacked = sizeof(MaskT) == 4 && sizeof(AccT) == 4;
+  uint64_t* myhd = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kChunk * 32 + lane;
 
   const long long U = (long long)groups * n;
   long long u = U * blockIdx.x / gridDim.x;
@@ -253,8 +258,13 @@ __global__ void __launch_bounds__(512, 1)
           if (h) {
             // kDepth: the 1-based stopping column k* instead of the cost
             // (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
-            myh[j * 32] = h;
-            myd[j * 32] = kDepth ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
+            const AccT dval = kDepth ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
+            if constexpr (kPacked) {
+              myhd[j * 32] = (uint64_t)h | ((uint64_t)dval << 32);
+            } else {
+              myh[j * 32] = h;
+              myd[j * 32] = dval;
+            }
             colmask |= 1u << j;
           }
         }
@@ -264,8 +274,14 @@ __global__ void __launch_bounds__(512, 1)
           if (h == 0) {
             const int j = __ffs(colmask) - 1;
             colmask &= colmask - 1;
-            h = myh[j * 32];
-            dv = myd[j * 32];
+            if constexpr (kPacked) {
+              const uint64_t x = myhd[j * 32];
+              h = (MaskT)x;
+              dv = (AccT)(x >> 32);
+            } else {
+              h = myh[j * 32];
+              dv = myd[j * 32];
+            }
           }
           const int c = Ops::pop_high(h);
           myacc[c * 32] += dv;
@@ -370,7 +386,7 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
           pass == 0 && (unsigned long long)std::min<long long>(seg, t.n) * vmax < (1ull << 32);
       if (pass == 0 && !acc32) continue;
       const size_t smem = scan_smem(t.m, sh.warps, acc32, sh.tsmem, sh.G);
-      const size_t inflight = (size_t)sh.warps * 32 * 2 * chunk_bytes;  // L1 room for prefetches
+      const size_t inflight = (size_t)sh.warps * 32 * chunk_bytes;  // L1 room for in-flight row loads
       if (smem <= max_smem && (fG || !sh.tsmem || smem + inflight <= l1_total)) {
         sp.G = sh.G;
         sp.tsmem = sh.tsmem;

@@ -1,6 +1,8 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+exec > gpurun_out/timing.log 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu -k "parity or smoke" 2>&1 | tail -1
+python tools/time_eval.py syn20k scan 10 "auto 32,14 32,12 32,10" 1
+python tools/time_eval.py syn5k scan 10 "auto 32,14" 1
+python tools/time_eval.py sweep:100 scan 10 "auto" 1
+python tools/time_eval.py pmed40 scan 10 "auto" 1
