@@ -133,10 +133,11 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   const size_t cells = n * (size_t)bp.Wp;
   PM_CUDA_TRY(c, c->ord.ensure(cells * bp.site_bytes));
   PM_CUDA_TRY(c, c->dist.ensure(cells * bp.dist_bytes));
-  PM_CUDA_TRY(c, c->dT.ensure(n * m * (size_t)bp.dist_bytes));
+  const size_t nP = (n + 15) / 16 * 16;
+  PM_CUDA_TRY(c, c->dT.ensure(nP * m * (size_t)bp.dist_bytes));
   PM_CUDA_TRY(c, launch_build_rows(bp, dcosts, c->ord.p, c->dist.p, c->sort_keys.p,
                                    c->sort_pay.as<uint32_t>(), c->stream));
-  PM_CUDA_TRY(c, launch_transpose_costs(dcosts, (int)n, (int)m, bp.dist_bytes, c->dT.p, c->stream));
+  PM_CUDA_TRY(c, launch_transpose_costs(dcosts, (int)n, (int)nP, (int)m, bp.dist_bytes, c->dT.p, c->stream));
   c->launches += 2;
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (!bp.smem_path) {
@@ -157,6 +158,7 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   t.ord = c->ord.p;
   t.dist = c->dist.p;
   t.dT = c->dT.p;
+  t.nP = (int)((n + 15) / 16 * 16);
   c->open_cap = (int)std::min<size_t>(m, (std::max<size_t>(p, 16) + 3) / 4 * 4);
   c->has_instance = true;
   c->err.clear();
@@ -240,7 +242,7 @@ static bool scan_fits(pm_ctx* c, size_t count) {
 // columns per client, the gather p sites.
 static int auto_kind(pm_ctx* c, size_t count) {
   if (!scan_fits(c, count)) return PM_EVAL_GATHER;
-  const double pstar = 1.3 * std::sqrt((double)c->t.m);
+  const double pstar = 1.05 * std::sqrt((double)c->t.m);
   return (double)c->t.p >= pstar ? PM_EVAL_SCAN : PM_EVAL_GATHER;
 }
 

@@ -386,7 +386,7 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
           pass == 0 && (unsigned long long)std::min<long long>(seg, t.n) * vmax < (1ull << 32);
       if (pass == 0 && !acc32) continue;
       const size_t smem = scan_smem(t.m, sh.warps, acc32, sh.tsmem, sh.G);
-      const size_t inflight = (size_t)sh.warps * 32 * chunk_bytes;  // L1 room for in-flight row loads
+      const size_t inflight = (size_t)sh.warps * 32 * chunk_bytes / 2;  // L1 room for in-flight row loads
       if (smem <= max_smem && (fG || !sh.tsmem || smem + inflight <= l1_total)) {
         sp.G = sh.G;
         sp.tsmem = sh.tsmem;
@@ -459,112 +459,114 @@ __global__ void __launch_bounds__(256) k_open_lists(const uint64_t* __restrict__
 }
 
 constexpr int kGatherThreads = 256;
-constexpr int kGatherR = 4;  // clients per thread
+
+// V consecutive clients per thread through one 16-byte load per open site.
+template <class DistT>
+struct GVec {
+  static constexpr int V = 16 / sizeof(DistT);
+  uint4 v;
+  __device__ __forceinline__ void set_max() { v = make_uint4(~0u, ~0u, ~0u, ~0u); }
+  __device__ __forceinline__ void min_with(const uint4 o) {
+    if constexpr (sizeof(DistT) == 2) {
+      v.x = __vminu2(v.x, o.x);
+      v.y = __vminu2(v.y, o.y);
+      v.z = __vminu2(v.z, o.z);
+      v.w = __vminu2(v.w, o.w);
+    } else if constexpr (sizeof(DistT) == 4) {
+      v.x = min(v.x, o.x);
+      v.y = min(v.y, o.y);
+      v.z = min(v.z, o.z);
+      v.w = min(v.w, o.w);
+    } else {
+      const uint64_t a0 = (uint64_t)v.x | ((uint64_t)v.y << 32), b0 = (uint64_t)o.x | ((uint64_t)o.y << 32);
+      const uint64_t a1 = (uint64_t)v.z | ((uint64_t)v.w << 32), b1 = (uint64_t)o.z | ((uint64_t)o.w << 32);
+      const uint64_t m0 = a0 < b0 ? a0 : b0, m1 = a1 < b1 ? a1 : b1;
+      v = make_uint4((uint32_t)m0, (uint32_t)(m0 >> 32), (uint32_t)m1, (uint32_t)(m1 >> 32));
+    }
+  }
+  __device__ __forceinline__ uint64_t elem(int q) const {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
+    if constexpr (sizeof(DistT) == 2) return (w[q >> 1] >> ((q & 1) * 16)) & 0xffffu;
+    else if constexpr (sizeof(DistT) == 4) return w[q];
+    else return (uint64_t)w[2 * q] | ((uint64_t)w[2 * q + 1] << 32);
+  }
+};
 
 template <class DistT, class OrdT>
 __global__ void __launch_bounds__(kGatherThreads)
-    k_gather(const DistT* __restrict__ dT, const OrdT* __restrict__ ord, const DistT* __restrict__ dist,
-             int n, int m, int p, int W, int Wp, const uint64_t* __restrict__ words, int wp,
-             const uint32_t* __restrict__ lists, const uint32_t* __restrict__ counts, int cap,
-             size_t count, int chunk, unsigned long long* __restrict__ costs,
-             unsigned long long* __restrict__ err, int mode) {
+    k_gather(const DistT* __restrict__ dT, int nP, const OrdT* __restrict__ ord,
+             const DistT* __restrict__ dist, int n, int m, int p, int W, int Wp,
+             const uint64_t* __restrict__ words, int wp, const uint32_t* __restrict__ lists,
+             const uint32_t* __restrict__ counts, int cap, size_t count, int chunk,
+             unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err, int mode) {
+  using Vec = GVec<DistT>;
+  constexpr int V = Vec::V;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* part = reinterpret_cast<unsigned long long*>(smem);  // [warps][chunk]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kWarps = kGatherThreads / 32;
   const size_t cbase = (size_t)blockIdx.y * chunk;
   const int cn = (int)min((size_t)chunk, count - cbase);
-
-  int ci[kGatherR];
-  uint64_t dlast[kGatherR];
-  uint32_t jlast[kGatherR];
-#pragma unroll
-  for (int r = 0; r < kGatherR; ++r) {
-    ci[r] = blockIdx.x * kGatherThreads * kGatherR + r * kGatherThreads + tid;
-    dlast[r] = 0;
-    jlast[r] = 0;
-    if (mode == 0 && ci[r] < n) {
-      dlast[r] = (uint64_t)dist[(size_t)ci[r] * Wp + (W - 1)];
-      jlast[r] = (uint32_t)ord[(size_t)ci[r] * Wp + (W - 1)];
-    }
-  }
-  const uint64_t kMax = ~0ull;
+  const int i0 = (blockIdx.x * kGatherThreads + tid) * V;  // first client of this thread
+  const int nv = i0 < n ? min(V, n - i0) : 0;               // real clients among the V
+  const DistT* col = dT + i0;
 
   for (int cl = 0; cl < cn; ++cl) {
     const size_t c = cbase + cl;
     const uint32_t pc = counts[c];
     unsigned long long sum = 0;
     if (pc == 0) {
-      if (tid == 0) atomicMin(err, (unsigned long long)c);
+      if (tid == 0 && blockIdx.x == 0) atomicMin(err, (unsigned long long)c);
     } else if (pc <= (uint32_t)cap && !(mode == 0 && pc < (uint32_t)p)) {
-      // common case: plain gather-min over the open list
-      uint64_t best[kGatherR];
+      // common case: min over the open list, V clients per 16-byte load
+      Vec best;
+      best.set_max();
+      if (nv > 0) {
+        const uint32_t* list = lists + c * (size_t)cap;
+        uint32_t t = 0;
+        for (; t + 4 <= pc; t += 4) {
+          uint4 x[4];
 #pragma unroll
-      for (int r = 0; r < kGatherR; ++r) best[r] = kMax;
-      const uint32_t* list = lists + c * (size_t)cap;
-      uint32_t t = 0;
-      for (; t + 4 <= pc; t += 4) {
-        uint32_t j[4];
+          for (int u = 0; u < 4; ++u)
+            x[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)__ldg(list + t + u) * nP));
 #pragma unroll
-        for (int x = 0; x < 4; ++x) j[x] = __ldg(list + t + x);
+          for (int u = 0; u < 4; ++u) best.min_with(x[u]);
+        }
+        for (; t < pc; ++t) best.min_with(__ldg(reinterpret_cast<const uint4*>(col + (size_t)__ldg(list + t) * nP)));
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int r = 0; r < kGatherR; ++r)
-            if (ci[r] < n) {
-              const uint64_t v = (uint64_t)dT[(size_t)j[x] * n + ci[r]];
-              best[r] = v < best[r] ? v : best[r];
-            }
+        for (int q = 0; q < V; ++q)
+          if (q < nv) sum += best.elem(q);
       }
-      for (; t < pc; ++t) {
-        const uint32_t j = __ldg(list + t);
-#pragma unroll
-        for (int r = 0; r < kGatherR; ++r)
-          if (ci[r] < n) {
-            const uint64_t v = (uint64_t)dT[(size_t)j * n + ci[r]];
-            best[r] = v < best[r] ? v : best[r];
-          }
-      }
-#pragma unroll
-      for (int r = 0; r < kGatherR; ++r)
-        if (ci[r] < n) sum += best[r];
     } else {
       // general path: walk the words in site order, track the (cost, site)
-      // minimum and, under the fitness contract with fewer than p open sites,
-      // check it sorts within the first W columns (ordering.cpp:50-52).
-      uint64_t best[kGatherR];
-      uint32_t bj[kGatherR];
-#pragma unroll
-      for (int r = 0; r < kGatherR; ++r) {
-        best[r] = kMax;
-        bj[r] = 0;
-      }
-      const uint64_t* w = words + c * wp;
-      for (int wi = 0; wi < wp; ++wi) {
-        uint64_t x = __ldg(w + wi);
-        if (wi == wp - 1 && (m & 63)) x &= (1ull << (m & 63)) - 1;
-        while (x) {
-          const uint32_t j = wi * 64 + (__ffsll((long long)x) - 1);
-          x &= x - 1;
-#pragma unroll
-          for (int r = 0; r < kGatherR; ++r)
-            if (ci[r] < n) {
-              const uint64_t v = (uint64_t)dT[(size_t)j * n + ci[r]];
-              if (v < best[r]) {  // strict: ascending j keeps the lowest site on ties
-                best[r] = v;
-                bj[r] = j;
-              }
-            }
-        }
-      }
+      // minimum per client and, under the fitness contract with fewer than p
+      // open sites, check it sorts within the first W columns (ordering.cpp:50-52).
       bool bad = false;
-#pragma unroll
-      for (int r = 0; r < kGatherR; ++r)
-        if (ci[r] < n) {
-          sum += best[r];
-          if (mode == 0 && pc < (uint32_t)p)
-            bad |= !(best[r] < dlast[r] || (best[r] == dlast[r] && bj[r] <= jlast[r]));
+      for (int q = 0; q < nv; ++q) {
+        const int i = i0 + q;
+        uint64_t best = ~0ull;
+        uint32_t bj = 0;
+        const uint64_t* w = words + c * wp;
+        for (int wi = 0; wi < wp; ++wi) {
+          uint64_t x = __ldg(w + wi);
+          if (wi == wp - 1 && (m & 63)) x &= (1ull << (m & 63)) - 1;
+          while (x) {
+            const uint32_t j = wi * 64 + (__ffsll((long long)x) - 1);
+            x &= x - 1;
+            const uint64_t v = (uint64_t)dT[(size_t)j * nP + i];
+            if (v < best) {  // strict: ascending j keeps the lowest site on ties
+              best = v;
+              bj = j;
+            }
+          }
         }
+        sum += best;
+        if (mode == 0 && pc < (uint32_t)p) {
+          const uint64_t dlast = (uint64_t)dist[(size_t)i * Wp + (W - 1)];
+          const uint32_t jlast = (uint32_t)ord[(size_t)i * Wp + (W - 1)];
+          bad |= !(best < dlast || (best == dlast && bj <= jlast));
+        }
+      }
       if (__any_sync(kFull, bad) && lane == 0) atomicMin(err, (unsigned long long)c);
     }
     sum = warp_sum(sum);
@@ -584,14 +586,15 @@ static cudaError_t launch_gather_t(const DevTables& t, const uint64_t* words, si
                                    const uint32_t* lists, const uint32_t* counts, int cap,
                                    unsigned long long* costs, unsigned long long* err, int mode,
                                    int sms, cudaStream_t st) {
-  const int xblocks = (t.n + kGatherThreads * kGatherR - 1) / (kGatherThreads * kGatherR);
-  // enough CTAs for ~4 waves of 4 resident CTAs per SM
-  long long want = (long long)sms * 16;
-  int chunk = (int)std::max<long long>(1, std::min<long long>(256, (long long)count * xblocks / want));
+  constexpr int V = 16 / sizeof(DistT);
+  const int xblocks = (t.n + kGatherThreads * V - 1) / (kGatherThreads * V);
+  // enough CTAs for ~8 resident CTAs per SM
+  const long long want = (long long)sms * 8;
+  const int chunk = (int)std::max<long long>(1, std::min<long long>(256, (long long)count * xblocks / want));
   const unsigned yblocks = (unsigned)((count + chunk - 1) / chunk);
   const size_t smem = (size_t)(kGatherThreads / 32) * chunk * 8;
   k_gather<DistT, OrdT><<<dim3(xblocks, yblocks), kGatherThreads, smem, st>>>(
-      (const DistT*)t.dT, (const OrdT*)t.ord, (const DistT*)t.dist, t.n, t.m, t.p, t.W, t.Wp, words,
+      (const DistT*)t.dT, t.nP, (const OrdT*)t.ord, (const DistT*)t.dist, t.n, t.m, t.p, t.W, t.Wp, words,
       wp, lists, counts, cap, count, chunk, costs, err, mode);
   return cudaGetLastError();
 }

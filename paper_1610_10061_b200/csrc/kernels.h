@@ -26,7 +26,7 @@ cudaError_t launch_validate_costs(const int64_t* costs, size_t count, unsigned l
                               int* out_neg, int sms, cudaStream_t st);
 cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
                               void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st);
-cudaError_t launch_transpose_costs(const int64_t* costs, int n, int m, int dist_bytes, void* dT,
+cudaError_t launch_transpose_costs(const int64_t* costs, int n, int nP, int m, int dist_bytes, void* dT,
                                    cudaStream_t st);
 
 // Device-resident tables as the evaluation kernels see them.
@@ -36,7 +36,8 @@ struct DevTables {
   int64_t max_cost = 0;
   const void* ord = nullptr;   // n x Wp, OrdT
   const void* dist = nullptr;  // n x Wp, DistT (sorted costs)
-  const void* dT = nullptr;    // m x n, DistT (site-major costs, gather kernel)
+  const void* dT = nullptr;    // m x nP, DistT (site-major costs, gather kernel)
+  int nP = 0;                  // dT row stride: round_up(n, 16)
 };
 
 // K2t: population words -> per-group transposed site masks T[g][s] (64 chromosomes / group).

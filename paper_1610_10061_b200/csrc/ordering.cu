@@ -230,8 +230,10 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 
 // ---- site-major narrow cost matrix for the gather-min kernel (K2b) --------
 
+// dT row stride nP = round_up(n, 16): 16-byte vector loads of consecutive
+// clients stay aligned; pad columns are written as 0 (never summed).
 template <class DistT>
-__global__ void k_transpose_costs(const int64_t* __restrict__ costs, int n, int m,
+__global__ void k_transpose_costs(const int64_t* __restrict__ costs, int n, int nP, int m,
                                   DistT* __restrict__ dT) {
   __shared__ int64_t tile[32][33];
   const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
@@ -243,7 +245,7 @@ __global__ void k_transpose_costs(const int64_t* __restrict__ costs, int n, int 
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
     const int j = j0 + r, i = i0 + tx;
-    if (i < n && j < m) dT[(size_t)j * n + i] = (DistT)tile[tx][r];
+    if (i < nP && j < m) dT[(size_t)j * nP + i] = i < n ? (DistT)tile[tx][r] : (DistT)0;
   }
 }
 
@@ -306,12 +308,12 @@ cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* o
   return launch_rows_od<uint32_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
 }
 
-cudaError_t launch_transpose_costs(const int64_t* costs, int n, int m, int dist_bytes, void* dT,
+cudaError_t launch_transpose_costs(const int64_t* costs, int n, int nP, int m, int dist_bytes, void* dT,
                                    cudaStream_t st) {
-  dim3 grid((m + 31) / 32, (n + 31) / 32), block(32, 8);
-  if (dist_bytes == 2) k_transpose_costs<uint16_t><<<grid, block, 0, st>>>(costs, n, m, (uint16_t*)dT);
-  else if (dist_bytes == 4) k_transpose_costs<uint32_t><<<grid, block, 0, st>>>(costs, n, m, (uint32_t*)dT);
-  else k_transpose_costs<uint64_t><<<grid, block, 0, st>>>(costs, n, m, (uint64_t*)dT);
+  dim3 grid((m + 31) / 32, (nP + 31) / 32), block(32, 8);
+  if (dist_bytes == 2) k_transpose_costs<uint16_t><<<grid, block, 0, st>>>(costs, n, nP, m, (uint16_t*)dT);
+  else if (dist_bytes == 4) k_transpose_costs<uint32_t><<<grid, block, 0, st>>>(costs, n, nP, m, (uint32_t*)dT);
+  else k_transpose_costs<uint64_t><<<grid, block, 0, st>>>(costs, n, nP, m, (uint64_t*)dT);
   return cudaGetLastError();
 }
 
