@@ -6,22 +6,23 @@
 // client i's ordered sites until the first open one (k*_i) and adds the
 // increments up to and including it; that prefix sum is dist[i][k*_i].
 //
-// K2 ("scan", bit-sliced).  64 chromosomes form a group.  The group's open
-// sets are transposed into T[s] (u64; bit c = chromosome c has site s open),
+// K2 ("scan", bit-sliced).  32 (or 64) chromosomes form a group.  The group's
+// open sets are transposed into T[s] (bit c = chromosome c has site s open),
 // staged in shared memory.  Each lane owns one client at a time and walks its
 // row once for the whole group: alive &= ~T[pi_ik], and every bit leaving
 // `alive` at column k is a (chromosome, client) pair whose cost is dist[i][k].
-// One row walk of length max_c k*_ic serves 64 evaluations, so a row prefix is
-// read from L2/HBM once per group instead of once per chromosome; lanes claim
-// clients dynamically so a short row does not wait for a long one.  Hits are
-// accumulated into per-lane private shared-memory counters (no atomics) and
+// One row walk of length max_c k*_ic serves the whole group, so a row prefix
+// is read from L2/HBM once per group instead of once per chromosome; lanes
+// claim clients dynamically so a short row does not wait for a long one.  Hits
+// are accumulated into per-lane private shared-memory counters (no atomics) and
 // reduced once per CTA segment.
 //
 // K2b ("gather", gather-min).  fitness = sum_i min_{j open} cost(i, j)
-// (instance.cpp:32-48, equal to the scan by acceptance.cpp:86-116).  Lanes are
-// clients; each open site j of a chromosome is one coalesced read of the
-// site-major row dT[j][i0..].  Wins when p is small (the scan reads ~m/p
-// columns per client, the gather p).  The reference's scan-width contract
+// (instance.cpp:32-48, equal to the scan by acceptance.cpp:86-116).  A thread
+// owns 16 bytes of consecutive clients (8 at u16 costs); each open site j of a
+// chromosome is one 16-byte read of the site-major row dT[j][i0..] and a packed
+// min.  Wins when p is small (the scan reads ~m/p columns per client, the
+// gather p): AUTO picks the scan iff p >= 1.05 sqrt(m), measured.  The reference's scan-width contract
 // (ordering.cpp:50-52) is enforced exactly: with popcount >= p it cannot fail
 // (W = m-p+1 columns always contain one of p distinct sites); with fewer open
 // sites the (cost, site)-smallest open site must not sort after column W-1.

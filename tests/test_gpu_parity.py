@@ -150,7 +150,8 @@ def test_empty_population_and_garbage_top_bits(ctx, oracle):
         assert (_eval(ctx, dirty, kind) == want).all()
 
 
-@pytest.mark.parametrize("npts,p,count", [(5000, 50, 1024), (20000, 200, 4096)])
+@pytest.mark.parametrize("npts,p,count", [(5000, 50, 1024), (20000, 200, 4096), (10000, 10, 512),
+                                          (10000, 1000, 512), (900, 90, 15360)])
 def test_baseline_sizes_scan_equals_gather(ctx, oracle, npts, p, count):
     """BASELINE configs syn5k / syn20k at full size: the two independent kernels
     agree on every chromosome, and sampled chromosomes equal the oracle's
