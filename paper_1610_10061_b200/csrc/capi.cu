@@ -37,11 +37,12 @@ int pm_create(int device, pm_ctx** out) {
     return PM_CUDA;
   }
   c->stream = c->own;
-  if (c->errw.ensure(16) != cudaSuccess) {
+  if (c->errw.ensure(kErrSlots * 8) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return PM_CUDA;
   }
-  cudaMemsetAsync(c->errw.p, 0xff, 16, c->stream);
+  cudaMemsetAsync(c->errw.p, 0xff, kErrSlots * 8, c->stream);
   *out = c;
   return PM_OK;
 }
@@ -58,6 +59,8 @@ void pm_destroy(pm_ctx* c) {
       cudaEventDestroy(e.first);
       cudaEventDestroy(e.second);
     }
+  for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
 }
@@ -256,11 +259,12 @@ int pm_auto_eval_kernel(pm_ctx* c) {
 }  // extern "C"
 
 namespace pmb {
-int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcosts, int mode) {
+int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcosts, int mode,
+                  unsigned long long* errw_override) {
   const DevTables& t = c->t;
   const int wp = (t.m + 63) / 64;
   PM_CUDA_TRY(c, cudaMemsetAsync(dcosts, 0, count * 8, c->stream));
-  unsigned long long* errw = c->errw.as<unsigned long long>();
+  unsigned long long* errw = errw_override ? errw_override : c->errw.as<unsigned long long>();
   int kind = c->eval_kind == PM_EVAL_AUTO ? auto_kind(c, count) : c->eval_kind;
   if (mode == 1) kind = PM_EVAL_GATHER;
   if (mode == 2) kind = PM_EVAL_SCAN;
@@ -342,6 +346,10 @@ int pm_evaluate_device(pm_ctx* c, const uint64_t* bitsets_device, size_t count, 
   return evaluate_dev(c, bitsets_device, count, words_per, costs_out_device, first_bad, 0);
 }
 
+// Host-buffer calls: the population is copied in chunks on a copy stream and
+// each chunk is evaluated on the compute stream as soon as it lands, so the
+// H2D transfer overlaps the kernels; costs and the per-chunk error words come
+// back with one synchronisation.
 static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_t words_per,
                          int64_t* costs_out, size_t* first_bad, int mode) {
   if (!c) return PM_STRUCTURAL;
@@ -351,17 +359,41 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
   PM_CUDA_TRY(c, cudaSetDevice(c->device));
   PM_CUDA_TRY(c, c->words.ensure(count * words_per * 8));
   PM_CUDA_TRY(c, c->costs_out.ensure(count * 8));
-  PM_CUDA_TRY(c, cudaMemcpyAsync(c->words.p, bitsets, count * words_per * 8, cudaMemcpyHostToDevice,
-                                 c->stream));
-  size_t fb = 0;
-  int rc = evaluate_dev(c, c->words.as<uint64_t>(), count, words_per, c->costs_out.as<int64_t>(), &fb, mode);
-  if (rc == PM_CONTRACT) {
-    if (first_bad) *first_bad = fb;
-    return rc;
+  // chunks of whole 64-chromosome groups; small batches go in one piece
+  // Measured on B200: each extra launch costs a CTA-segment tail, which
+  // outweighs the overlap until a chunk carries >= 8192 chromosomes and
+  // >= 16 MB of words (the BASELINE batches stay in one piece).
+  const size_t bytes = count * words_per * 8;
+  const int chunks = (int)std::max<size_t>(
+      1, std::min<size_t>({(size_t)kErrSlots - 1, count / 8192, bytes / (16u << 20)}));
+  const size_t per = ((count + chunks - 1) / chunks + 63) / 64 * 64;
+  while ((int)c->chunk_ev.size() < chunks) {
+    cudaEvent_t e;
+    PM_CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->chunk_ev.push_back(e);
   }
-  if (rc != PM_OK) return rc;
+  unsigned long long* slots = c->errw.as<unsigned long long>() + 1;
+  PM_CUDA_TRY(c, cudaMemsetAsync(slots, 0xff, chunks * 8, c->stream));
+  int used = 0;
+  for (size_t off = 0; off < count; off += per, ++used) {
+    const size_t cnt = std::min(per, count - off);
+    PM_CUDA_TRY(c, cudaMemcpyAsync(c->words.as<uint64_t>() + off * words_per, bitsets + off * words_per,
+                                   cnt * words_per * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    PM_CUDA_TRY(c, cudaEventRecord(c->chunk_ev[used], c->copy_stream));
+    PM_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->chunk_ev[used], 0));
+    const int rc = evaluate_core(c, c->words.as<uint64_t>() + off * words_per, cnt,
+                                 c->costs_out.as<int64_t>() + off, mode, slots + used);
+    if (rc != PM_OK) return rc;
+  }
+  std::vector<unsigned long long> errs(used);
   PM_CUDA_TRY(c, cudaMemcpyAsync(costs_out, c->costs_out.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(errs.data(), slots, used * 8, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < used; ++i)
+    if (errs[i] != ~0ull) {
+      if (first_bad) *first_bad = (size_t)i * per + (size_t)errs[i];
+      return c->fail(PM_CONTRACT, mode == 1 ? kMsgNoneOpen : kMsgRunoff);
+    }
   return PM_OK;
 }
 

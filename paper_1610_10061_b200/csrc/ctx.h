@@ -13,6 +13,7 @@
 namespace pmb {
 
 // Reference message texts (errors thrown by the code each status replaces).
+inline constexpr int kErrSlots = 8;  // error words: [0] the context's, [1..] pipelined chunks
 inline constexpr const char* kMsgLength = "chromosome length must equal the site count";  // ordering.cpp:42
 inline constexpr const char* kMsgRunoff =
     "no open site within the scan width; exactly p sites must be open";  // ordering.cpp:51
@@ -65,6 +66,8 @@ struct pm_ctx {
   // scratch
   DevBuf costs_in, sort_keys, sort_pay, words, costs_out, T, lists, counts, errw, scal;
   int open_cap = 0;
+  cudaStream_t copy_stream = nullptr;  // H2D of pipelined host-buffer calls
+  std::vector<cudaEvent_t> chunk_ev;
 
   // kernel timing hook: events around the dominant evaluation kernel
   bool profiling = false;
@@ -100,5 +103,7 @@ struct pm_ctx {
 namespace pmb {
 // Fitness of `count` device-resident chromosomes into device costs (mode 0:
 // fitness, 1: min_cost_sum, 2: scan depths).  Asynchronous on ctx->stream.
-int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcosts, int mode);
+// errw: device word receiving the lowest failing index (nullptr: the context's).
+int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcosts, int mode,
+                  unsigned long long* errw = nullptr);
 }  // namespace pmb
