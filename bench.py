@@ -331,6 +331,8 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
     cfg = pm.ga_config(nb=nb, nt=256, evolve_limit=GA_GENS, saturation=GA_GENS + 1, seed=1,
                        population="device")
     ag = None if world == 1 else pm.torch_allgather(device=f"cuda:{local}")
+    warm = pm.ga_config(nb=nb, nt=256, evolve_limit=1, saturation=1, seed=2, population="device")
+    ctx.run_ga(warm, rank=rank, world=world, allgather=ag)  # first launches load the GA kernels
     r = ctx.run_ga(cfg, rank=rank, world=world, allgather=ag)
     out["islands"] = {"config": f"n=m={n}, p={p}, nb={nb} ({16} per GPU), nt=256, device population draw",
                       "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
@@ -345,6 +347,7 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
         for pop_mode in ("reference", "device"):
             cfg = pm.ga_config(nb=60, nt=256, evolve_limit=GA_GENS, saturation=GA_GENS + 1, seed=1,
                                population=pop_mode)
+            c2.run_ga(pm.ga_config(nb=60, nt=256, evolve_limit=1, saturation=1, seed=2, population=pop_mode))
             r = c2.run_ga(cfg)
             out[f"pmed40_shape_{pop_mode}_population"] = {
                 "config": "synthetic Euclidean n=m=900, p=90, nb=60, nt=256 (OR-Library pmed40 absent)",

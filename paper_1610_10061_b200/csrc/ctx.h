@@ -48,6 +48,14 @@ using pmb::DevBuf;
 using pmb::DevTables;
 using pmb::BuildPlan;
 
+namespace pmb {
+// GA working set (ga.cu), grow-only and kept across calls.
+struct GaBuffers {
+  DevBuf pop, next, cost, before, child, ccost, ok, bcost, bthread, bwords, evals, tmp;
+};
+}  // namespace pmb
+using pmb::GaBuffers;
+
 struct pm_ctx {
   int device = 0;
   int sms = 148;
@@ -66,6 +74,7 @@ struct pm_ctx {
   // scratch
   DevBuf costs_in, sort_keys, sort_pay, words, costs_out, T, lists, counts, errw, scal;
   int open_cap = 0;
+  GaBuffers ga;
   cudaStream_t copy_stream = nullptr;  // H2D of pipelined host-buffer calls
   std::vector<cudaEvent_t> chunk_ev;
 

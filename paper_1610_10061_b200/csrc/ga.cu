@@ -199,9 +199,6 @@ static unsigned cdiv(size_t a, unsigned b) { return (unsigned)((a + b - 1) / b);
 
 // ---- GA engine ---------------------------------------------------------------------
 
-struct GaBuffers {
-  DevBuf pop, next, cost, before, child, ccost, ok, bcost, bthread, bwords, evals, tmp;
-};
 
 struct GaShape {
   int nbl = 0, nt = 0, wp = 0, m = 0, p = 0, rounds = 0, attempts = 0, cycle = 0;
@@ -278,11 +275,6 @@ static int ga_alloc(pm_ctx* c, GaBuffers& B, const GaShape& s) {
   return PM_OK;
 }
 
-static void ga_release(GaBuffers& B) {
-  for (DevBuf* b : {&B.pop, &B.next, &B.cost, &B.before, &B.child, &B.ccost, &B.ok, &B.bcost, &B.bthread,
-                    &B.bwords, &B.evals, &B.tmp})
-    b->release();
-}
 
 // GaConfig::validate (ga.cpp:25-33), same texts.
 static int validate_config(pm_ctx* c, const pm_ga_config* cfg) {
@@ -364,7 +356,7 @@ int pm_evolve_blocks(pm_ctx* c, uint64_t* blocks, size_t nb, size_t words_per, c
   if (words_per != (size_t)(c->t.m + 63) / 64) return c->fail(PM_STRUCTURAL, kMsgLength);
   if (nb == 0) return PM_OK;
   PM_CUDA_TRY(c, cudaSetDevice(c->device));
-  GaBuffers B;
+  GaBuffers& B = c->ga;  // grow-only, kept across calls
   const GaShape s = make_shape(c, cfg, nb, first_block);
   rc = ga_alloc(c, B, s);
   if (rc) return rc;
@@ -378,14 +370,12 @@ int pm_evolve_blocks(pm_ctx* c, uint64_t* blocks, size_t nb, size_t words_per, c
   PM_CUDA_TRY(c, cudaMemcpyAsync(&bad, B.tmp.p, 8, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (bad != ~0ull) {
-    ga_release(B);
     return c->fail(PM_DOMAIN, "every chromosome of an evolved block must open exactly p sites");
   }
   PM_CUDA_TRY(c, cudaMemsetAsync(c->errw.p, 0xff, 8, c->stream));
   PM_CUDA_TRY(c, cudaMemsetAsync(B.evals.p, 0, 8, c->stream));
   rc = evolve_all(c, B, s, kernel_index);
   if (rc) {
-    ga_release(B);
     return rc;
   }
   std::vector<int64_t> bc(nb);
@@ -394,7 +384,6 @@ int pm_evolve_blocks(pm_ctx* c, uint64_t* blocks, size_t nb, size_t words_per, c
   PM_CUDA_TRY(c, cudaMemcpyAsync(bc.data(), B.bcost.p, nb * 8, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaMemcpyAsync(bt.data(), B.bthread.p, nb * 8, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  ga_release(B);
   size_t fb = 0;
   rc = pm_check_errors(c, &fb);
   if (rc) return rc;
@@ -417,7 +406,7 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
   PM_CUDA_TRY(c, cudaSetDevice(c->device));
   const auto t0 = std::chrono::steady_clock::now();
   const size_t nb = cfg->nb, nt = cfg->nt, nbl = nb / world, block0 = nbl * rank;
-  GaBuffers B;
+  GaBuffers& B = c->ga;  // grow-only, kept across calls
   const GaShape s = make_shape(c, cfg, nbl, block0);
   rc = ga_alloc(c, B, s);
   if (rc) return rc;
@@ -513,7 +502,6 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
   unsigned long long ref_evals = 0;
   PM_CUDA_TRY(c, cudaMemcpyAsync(&ref_evals, B.evals.p, 8, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  ga_release(B);
   size_t fb = 0;
   rc = pm_check_errors(c, &fb);
   if (rc) return rc;

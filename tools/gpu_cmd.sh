@@ -1,5 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -q -x -m gpu -k "parity or cpp" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --no-ga > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-for c in syn5k pmed40; do timeout 600 python bench.py --config $c --no-ga --no-cpu-baseline > gpurun_out/bench_$c.json 2>> gpurun_out/bench.err; done
+exec > gpurun_out/timing.log 2>&1
+python tools/prof_ga.py syn20k 3 device
+python tools/prof_ga.py pmed40 3 device
+python tools/prof_ga.py syn20k 2 device && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ga_launches.csv python tools/prof_ga.py syn20k 2 device > /dev/null 2>&1
