@@ -133,6 +133,18 @@ int pm_set_profiling(pm_ctx* ctx, int enabled);
  * launches since the last read, and resets. */
 int pm_profile_read(pm_ctx* ctx, double* kernel_ms, uint64_t* kernel_launches);
 
+/* ---- instance ingestion (proj/src/bench.cpp:65-168) ---------------------------
+ * OR-Library graph text ("n edges p" + "u v cost" triples): the reference's
+ * parse_orlib diagnostics (same texts), then the all-pairs shortest-path closure
+ * on the device (blocked Floyd-Warshall) and pm_set_instance_device on it.
+ * p_override != 0 replaces the file's p (run_benchmark's --p). */
+int pm_set_instance_orlib(pm_ctx* ctx, const char* text, size_t len, size_t p_override);
+/* The closure alone, copied to the host (n*n int64 into costs_out, capacity entries). */
+int pm_orlib_closure(pm_ctx* ctx, const char* text, size_t len, int64_t* costs_out, size_t capacity,
+                     size_t* n_out, size_t* p_out);
+/* Dense text ("n m p" + n rows of m costs): parse_dense diagnostics, then pm_set_instance. */
+int pm_set_instance_dense(pm_ctx* ctx, const char* text, size_t len, size_t p_override);
+
 /* ---- genetic algorithm (K3 evolve, K4 islands) ------------------------------ */
 
 enum { PM_MIGRATE_BLOCK = 0, PM_MIGRATE_TEAM = 1 }; /* MigrationMode, ga.hpp:22 */

@@ -81,6 +81,16 @@ class Oracle:
                                              _u64p, C.POINTER(_sz)]
         L.or_min_cost_sum.argtypes = [_sz, _sz, _i64p, _u64p, C.POINTER(C.c_int64)]
         L.or_direct_cost.argtypes = [_sz, _sz, _sz, _i64p, _u64p, C.POINTER(C.c_int64)]
+        L.or_orlib_closure.argtypes = [_sz, _sz, _i64p, _i64p, _i64p, C.POINTER(_sz)]
+
+    def orlib_closure(self, n, uv, w):
+        """uv: 0-based endpoints [edges, 2]; -> (rc, closure n*n, first bad index)"""
+        uv = np.ascontiguousarray(uv, dtype=np.int64).reshape(-1)
+        w = np.ascontiguousarray(w, dtype=np.int64)
+        out = np.zeros(n * n, dtype=np.int64)
+        bad = _sz(0)
+        rc = self.L.or_orlib_closure(n, w.size, uv if uv.size else np.zeros(2, np.int64), w if w.size else np.zeros(1, np.int64), out, C.byref(bad))
+        return rc, out, bad.value
 
     # rng.hpp
     def derive(self, master: int, key) -> int:
@@ -196,6 +206,15 @@ class RefLib:
                                  C.c_longlong, C.c_int, C.c_uint, _u64p, C.POINTER(C.c_int64),
                                  C.POINTER(_sz), C.POINTER(_sz), _i64p, C.POINTER(C.c_double)]
         L.ref_validate_config.argtypes = [_sz, _sz, _sz, _sz, C.c_int]
+        L.ref_parse.argtypes = [C.c_int, C.c_char_p, _i64p, _sz, C.POINTER(_sz), C.POINTER(_sz),
+                                C.POINTER(_sz)]
+
+    def parse(self, text: str, orlib: bool = True, cap: int = 1 << 22):
+        """parse_orlib / parse_dense -> (rc, n, m, p, costs)"""
+        out = np.zeros(cap, dtype=np.int64)
+        n, m, p = _sz(0), _sz(0), _sz(0)
+        rc = self.L.ref_parse(int(orlib), text.encode(), out, cap, C.byref(n), C.byref(m), C.byref(p))
+        return rc, n.value, m.value, p.value, out[: n.value * m.value].copy()
 
     def last_error(self) -> str:
         return self.L.ref_last_error().decode()

@@ -254,3 +254,33 @@ int or_direct_cost(size_t n, size_t m, size_t p, const int64_t* costs, const uin
   if (pc != p) return OR_CONTRACT;
   return or_min_cost_sum(n, m, costs, words, out);
 }
+
+/* ---- parse_orlib closure: src/bench.cpp:121-166 -------------------------
+ * uv: 2*edges 0-based endpoints, w: edge costs (already validated).  out: n*n.
+ * Returns OR_STRUCTURAL and the first unreachable pair (row-major) in *bad. */
+int or_orlib_closure(size_t n, size_t edges, const int64_t* uv, const int64_t* w, int64_t* out,
+                     size_t* bad) {
+  const int64_t kUnreachable = INT64_MAX / 4; /* bench.cpp:123 */
+  for (size_t x = 0; x < n * n; ++x) out[x] = kUnreachable;
+  for (size_t i = 0; i < n; ++i) out[i * n + i] = 0;
+  for (size_t e = 0; e < edges; ++e) { /* bench.cpp:141-143: cheapest parallel edge */
+    const size_t a = (size_t)uv[2 * e], b = (size_t)uv[2 * e + 1];
+    if (w[e] < out[a * n + b]) out[a * n + b] = w[e];
+    if (w[e] < out[b * n + a]) out[b * n + a] = w[e];
+  }
+  for (size_t k = 0; k < n; ++k) /* bench.cpp:146-157 */
+    for (size_t i = 0; i < n; ++i) {
+      const int64_t dik = out[i * n + k];
+      if (dik == kUnreachable) continue;
+      for (size_t j = 0; j < n; ++j) {
+        const int64_t t = dik + out[k * n + j];
+        if (t < out[i * n + j]) out[i * n + j] = t;
+      }
+    }
+  for (size_t x = 0; x < n * n; ++x) /* bench.cpp:159-166 */
+    if (out[x] >= kUnreachable) {
+      if (bad) *bad = x;
+      return OR_STRUCTURAL;
+    }
+  return OR_OK;
+}

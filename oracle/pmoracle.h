@@ -35,6 +35,9 @@ int or_min_cost_sum(size_t n, size_t m, const int64_t* costs, const uint64_t* wo
 int or_direct_cost(size_t n, size_t m, size_t p, const int64_t* costs, const uint64_t* words,
                    int64_t* out);
 
+int or_orlib_closure(size_t n, size_t edges, const int64_t* uv, const int64_t* w, int64_t* out,
+                     size_t* bad);
+
 #ifdef __cplusplus
 }
 #endif

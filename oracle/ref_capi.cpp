@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "pmedian/bench.hpp"
 #include "pmedian/combinatorics.hpp"
 #include "pmedian/errors.hpp"
 #include "pmedian/ga.hpp"
@@ -292,6 +293,19 @@ int ref_run_ga(void* h, std::size_t nb, std::size_t nt, std::size_t evolve_limit
     *kernel_of_best = r.kernel_of_best;
     for (std::size_t k = 0; k < r.per_kernel_best_costs.size(); ++k) per_kernel[k] = r.per_kernel_best_costs[k];
     *wall_s = r.wall_time.count();
+  });
+}
+
+// parse_orlib / parse_dense (bench.cpp:65-168): cost matrix out (cap entries), n/m/p out.
+int ref_parse(int orlib, const char* text, std::int64_t* costs_out, std::size_t cap, std::size_t* n,
+              std::size_t* m, std::size_t* p) {
+  return guard([&] {
+    const Instance inst = orlib ? parse_orlib(text) : parse_dense(text);
+    *n = inst.clients();
+    *m = inst.sites();
+    *p = inst.open_count();
+    if (costs_out && cap >= inst.costs().size())
+      std::memcpy(costs_out, inst.costs().data(), inst.costs().size() * 8);
   });
 }
 

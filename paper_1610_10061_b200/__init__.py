@@ -68,6 +68,9 @@ _lib.pm_evolve_blocks.argtypes = [_vp, _vp, _sz, _sz, C.POINTER(GaConfig), C.c_u
 _lib.pm_run_ga.argtypes = [_vp, C.POINTER(GaConfig), _vp, _vp, C.POINTER(_RunResult)]
 _lib.pm_run_ga_islands.argtypes = [_vp, C.POINTER(GaConfig), C.c_int, C.c_int, ALLGATHER_FN, _vp, _vp,
                                    _vp, C.POINTER(_RunResult)]
+_lib.pm_set_instance_orlib.argtypes = [_vp, C.c_char_p, _sz, _sz]
+_lib.pm_set_instance_dense.argtypes = [_vp, C.c_char_p, _sz, _sz]
+_lib.pm_orlib_closure.argtypes = [_vp, C.c_char_p, _sz, _vp, _sz, C.POINTER(_sz), C.POINTER(_sz)]
 MIGRATE_BLOCK, MIGRATE_TEAM = 0, 1
 POPULATION_REFERENCE, POPULATION_DEVICE = 0, 1
 
@@ -86,7 +89,8 @@ C_ABI_SYMBOLS = (
     "pm_set_instance", "pm_set_instance_device", "pm_table_info_get", "pm_get_tables",
     "pm_evaluate", "pm_evaluate_device", "pm_check_errors", "pm_set_eval_kernel",
     "pm_auto_eval_kernel", "pm_min_cost_sum", "pm_scan_depths_device", "pm_set_profiling",
-    "pm_profile_read", "pm_evolve_blocks", "pm_run_ga", "pm_run_ga_islands",
+    "pm_profile_read", "pm_evolve_blocks", "pm_run_ga", "pm_run_ga_islands", "pm_set_instance_orlib",
+    "pm_orlib_closure", "pm_set_instance_dense",
 )
 
 
@@ -252,6 +256,30 @@ class Context:
                 raise StructuralError("cost matrix must be exactly n rows by m columns")
             self._check(_lib.pm_set_instance_device(self._h, _ptr(costs), n, m, p))
         self.n, self.m, self.p = n, m, p
+
+    def set_instance_orlib(self, text: str, p: int = 0) -> None:
+        """parse_orlib (bench.cpp:106-168) with the closure on the device."""
+        b = text.encode()
+        self._check(_lib.pm_set_instance_orlib(self._h, b, len(b), p))
+        ti = self.table_info()
+        self.n, self.m, self.p = ti.clients, ti.sites, ti.open_count
+
+    def set_instance_dense(self, text: str, p: int = 0) -> None:
+        """parse_dense (bench.cpp:65-104)."""
+        b = text.encode()
+        self._check(_lib.pm_set_instance_dense(self._h, b, len(b), p))
+        ti = self.table_info()
+        self.n, self.m, self.p = ti.clients, ti.sites, ti.open_count
+
+    def orlib_closure(self, text: str):
+        """-> (n, p, costs int64 [n*n]) -- the graph's shortest-path closure."""
+        b = text.encode()
+        n, p = _sz(0), _sz(0)
+        self._check(_lib.pm_orlib_closure(self._h, b, len(b), None, 0, C.byref(n), C.byref(p)))
+        out = np.zeros(n.value * n.value, dtype=np.int64)
+        self._check(_lib.pm_orlib_closure(self._h, b, len(b), out.ctypes.data, out.size, C.byref(n),
+                                          C.byref(p)))
+        return n.value, p.value, out
 
     def table_info(self) -> TableInfo:
         ti = _TableInfo()
