@@ -186,3 +186,41 @@ def test_device_buffers_and_stream(ctx, oracle):
     assert ctx.kernel_launches > before
     assert (out.cpu().numpy() == want).all()
     ctx.set_stream(None)
+
+
+def test_payload_key_path_huge_costs(ctx, oracle):
+    """cost bits + site bits > 64: K1 sorts a u64 cost key with a separate site
+    payload; D' is u64.  Ties are frequent (few distinct huge values)."""
+    n, m, p = 7, 300, 11
+    base = oracle.random_costs(9, n, m, 5)
+    costs = (base.astype(np.int64) << np.int64(58)) // 7 + base  # ~2^60, many ties
+    ctx.set_instance(costs, n, m, p)
+    assert ctx.table_info().dist_bytes == 8
+    so, inc = oracle.build_ordering(n, m, p, costs)
+    so2, inc2 = ctx.get_tables()
+    assert (so == so2).all() and (inc == inc2).all()
+    pop = oracle.random_population(m, p, 100, seed=4)
+    want = oracle.evaluate(so, inc, m, pop)[1]
+    for kind in KINDS:
+        assert (_eval(ctx, pop, kind) == want).all()
+
+
+def test_pipelined_host_call_reports_global_first_bad(ctx, pm, oracle):
+    """pm_evaluate splits large host batches into overlapped chunks; costs and the
+    lowest failing index are still global."""
+    npts, p, count = 20000, 200, 16384
+    costs = oracle.synth_euclid(npts)
+    ctx.set_instance(costs, npts, npts, p)
+    pop = oracle.random_population(npts, p, count, seed=11)
+    good = ctx.evaluate(pop)
+    ctx.set_eval_kernel(pm.EVAL_GATHER)
+    assert (ctx.evaluate(pop) == good).all()
+    ctx.set_eval_kernel(pm.EVAL_AUTO)
+    for r in range(0, count, count // 4):
+        assert oracle.min_cost_sum(npts, npts, costs, pop[r]) == (0, good[r])
+    bad = pop.copy()
+    bad[12001] = 0
+    bad[15000] = 0
+    with pytest.raises(pm.ContractError) as ei:
+        ctx.evaluate(bad)
+    assert ei.value.first_bad == 12001
