@@ -111,15 +111,23 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# PMB_DIST_BACKEND=gloo and PMB_DEVICE=<d> let a multi-rank run share one GPU
+# for plumbing tests (host-side collectives only; no kernel waits on another rank).
+BACKEND = os.environ.get("PMB_DIST_BACKEND", "nccl")
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("PMB_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     if world > 1:
         import torch.distributed as dist
         import torch
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(BACKEND)
     return world, rank, local
 
 
@@ -128,7 +136,7 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if BACKEND == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -330,7 +338,7 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
     nb = 16 * world
     cfg = pm.ga_config(nb=nb, nt=256, evolve_limit=GA_GENS, saturation=GA_GENS + 1, seed=1,
                        population="device")
-    ag = None if world == 1 else pm.torch_allgather(device=f"cuda:{local}")
+    ag = None if world == 1 else pm.torch_allgather(device=f"cuda:{local}" if BACKEND == "nccl" else None)
     warm = pm.ga_config(nb=nb, nt=256, evolve_limit=1, saturation=1, seed=2, population="device")
     ctx.run_ga(warm, rank=rank, world=world, allgather=ag)  # first launches load the GA kernels
     r = ctx.run_ga(cfg, rank=rank, world=world, allgather=ag)

@@ -1,0 +1,26 @@
+"""bench.py's multi-rank path (torchrun, weak scaling, max-over-ranks timing,
+island GA allgather) end to end.  Two ranks share the one GPU over gloo: the
+collectives are host-side, so no kernel waits on another rank."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_gloo_one_gpu():
+    env = dict(os.environ, PMB_DIST_BACKEND="gloo", PMB_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--config", "syn5k", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 prints one line
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["ga"]["islands"]["generations"] >= 1
