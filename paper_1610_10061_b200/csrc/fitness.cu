@@ -98,6 +98,12 @@ struct Chunk {
 #pragma unroll
     for (int x = 0; x < kD; x += 2) ldg_stream32(reinterpret_cast<const uint4*>(drow + k) + x, d[x], d[x + 1]);
   }
+  // Every site of the chunk becomes `s` (the never-open sentinel site m).
+  __device__ __forceinline__ void set_sentinel(uint32_t s) {
+    const uint32_t w = sizeof(OrdT) == 2 ? (s | (s << 16)) : s;
+#pragma unroll
+    for (int x = 0; x < kO; ++x) o[x] = make_uint4(w, w, w, w);
+  }
   __device__ __forceinline__ uint32_t site(int j) const {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(o);
     if constexpr (sizeof(OrdT) == 2) return (w[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
@@ -167,11 +173,15 @@ __global__ void __launch_bounds__(512, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = lanemask_lt();
   AccT* myacc = acc + (size_t)warp * kG * 32 + lane;
-  MaskT* myh = hbuf + (size_t)warp * kChunk * 32 + lane;
-  AccT* myd = dbuf + (size_t)warp * kChunk * 32 + lane;
-  // 32-bit mask and 32-bit cost: park both in one 8-byte slot (one STS / LDS)
+  // the warp's queue of hit columns (at most kChunk * 32 per chunk); a 32-bit
+  // mask and a 32-bit cost share one 8-byte record (one STS / LDS)
   constexpr bool kPacked = sizeof(MaskT) == 4 && sizeof(AccT) == 4;
-  uint64_t* myhd = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kChunk * 32 + lane;
+  MaskT* wqh = hbuf + (size_t)warp * kChunk * 32;
+  AccT* wqd = dbuf + (size_t)warp * kChunk * 32;
+  uint64_t* wq = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kChunk * 32;
+  (void)wqh;
+  (void)wqd;
+  (void)wq;
 
   const long long U = (long long)groups * n;
   long long u = U * blockIdx.x / gridDim.x;
@@ -207,6 +217,12 @@ __global__ void __launch_bounds__(512, 1)
     const OrdT* orow = nullptr;
     const DistT* drow = nullptr;
     Chunk<OrdT, DistT> ca, cb, cc;
+    // T[Ts-1] is a zero mask (k_transpose_population clears [m, Ts)): idle
+    // lanes look it up and never hit
+    const uint32_t sentinel = (uint32_t)(Ts - 1);
+    ca.set_sentinel(sentinel);
+    cb.set_sentinel(sentinel);
+    cc.set_sentinel(sentinel);
     int wb_next = 0, wb_end = 0;
     bool exhausted = false;
 
@@ -244,53 +260,64 @@ __global__ void __launch_bounds__(512, 1)
         need = __ballot_sync(kFull, i < 0);
       }
       if (__ballot_sync(kFull, i >= 0) == 0) return false;
-      if (i >= 0) {
-        MaskT t[kChunk];
+      // Every lane runs the column phase (idle lanes hold sentinel sites and
+      // alive == 0), so the warp can append its hit columns to one queue with
+      // ballots instead of per-lane slots.
+      MaskT t[kChunk];
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          if constexpr (kTSmem) t[j] = Tsm[cur.site(j)];
-          else t[j] = (MaskT)(__ldg(Tg + cur.site(j)) >> half);
-        }
-        uint32_t colmask = 0;
+      for (int j = 0; j < kChunk; ++j) {
+        if constexpr (kTSmem) t[j] = Tsm[cur.site(j)];
+        else t[j] = (MaskT)(__ldg(Tg + cur.site(j)) >> half);
+      }
+      uint32_t qn = 0;  // warp-uniform queue length
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          const MaskT h = alive & t[j];
-          alive &= ~t[j];
-          if (h) {
-            // kDepth: the 1-based stopping column k* instead of the cost
-            // (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
-            const AccT dval = kDepth ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
-            if constexpr (kPacked) {
-              myhd[j * 32] = (uint64_t)h | ((uint64_t)dval << 32);
-            } else {
-              myh[j * 32] = h;
-              myd[j * 32] = dval;
-            }
-            colmask |= 1u << j;
+      for (int j = 0; j < kChunk; ++j) {
+        const MaskT h = alive & t[j];
+        alive &= ~t[j];
+        const unsigned hb = __ballot_sync(kFull, h != 0);
+        if (h) {
+          // kDepth: the 1-based stopping column k* instead of the cost
+          // (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
+          const AccT dval = kDepth ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
+          const uint32_t q = qn + __popc(hb & lt);
+          if constexpr (kPacked) {
+            wq[q] = (uint64_t)h | ((uint64_t)dval << 32);
+          } else {
+            wqh[q] = h;
+            wqd[q] = dval;
           }
         }
+        qn += __popc(hb);
+      }
+      // drain: lane r applies queue records r, r+32, ... -- the loop runs the
+      // largest record's bit count, not the busiest lane's hit count
+      for (uint32_t base = 0; base < qn; base += 32) {
         MaskT h = 0;
         AccT dv = 0;
-        while (colmask | (h != 0)) {
-          if (h == 0) {
-            const int j = __ffs(colmask) - 1;
-            colmask &= colmask - 1;
-            if constexpr (kPacked) {
-              const uint64_t x = myhd[j * 32];
-              h = (MaskT)x;
-              dv = (AccT)(x >> 32);
-            } else {
-              h = myh[j * 32];
-              dv = myd[j * 32];
-            }
+        if (base + lane < qn) {
+          if constexpr (kPacked) {
+            const uint64_t x = wq[base + lane];
+            h = (MaskT)x;
+            dv = (AccT)(x >> 32);
+          } else {
+            h = wqh[base + lane];
+            dv = wqd[base + lane];
           }
+        }
+        while (h) {
           const int c = Ops::pop_high(h);
           myacc[c * 32] += dv;
         }
+      }
+      if (i >= 0) {
         k += kChunk;
         if (alive == 0 || k >= Wp) {
           if (alive) atomicMin(err, (unsigned long long)g * kG + Ops::low_index(alive));
           i = -1;
+          alive = 0;
+          cur.set_sentinel(sentinel);
+          nxt.set_sentinel(sentinel);
+          nxt2.set_sentinel(sentinel);
         } else if (k + (kBufs - 1) * kChunk < Wp) {
           cur.load(orow, drow, k + (kBufs - 1) * kChunk);
         }
