@@ -81,17 +81,22 @@ class ClockSampler:
             h = nv.nvmlDeviceGetHandleByIndex(self.device)
             self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
 
+            def sample():
+                try:
+                    self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for bit, name in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+
             def run():
                 while not self._stop.is_set():
-                    try:
-                        self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
-                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        for bit, name in self.REASONS.items():
-                            if r & bit:
-                                self.reasons.add(name)
-                    except Exception:
-                        pass
+                    sample()
                     time.sleep(0.002)
+
+            self._sample = sample
 
             self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
@@ -100,6 +105,8 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        if getattr(self, "_sample", None):
+            self._sample()  # the region's end, even when it was shorter than a tick
         self._stop.set()
         if self.t:
             self.t.join(timeout=2)
