@@ -228,6 +228,139 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   }
 }
 
+// ---- K1 (packed keys): warp-slice stable LSD radix sort ---------------------
+//
+// Each of the 32 warps owns a contiguous slice of the row.  Per pass: every
+// warp histograms its slice (match_any leaders bump the warp's private
+// counters -- no atomics), one exclusive scan over (digit, warp) turns the
+// counts into scatter offsets, and every warp scatters its slice in order
+// (rank within a 32-element step from match_any, then the leader advances the
+// warp's offset).  Slices in warp order and steps in lane order keep the
+// pass stable; only 3 block barriers per pass.
+constexpr int kWsWarps = kSortThreads / 32;
+
+// Lanes holding the same digit (valid lanes only): one ballot per digit bit
+// (the warp multi-split trick) -- far cheaper than MATCH.ANY over 32 distinct
+// values, which the profile showed serialising.
+template <int kBits>
+__device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid) {
+  unsigned peers = __ballot_sync(kFull, valid);
+#pragma unroll
+  for (int b = 0; b < kBits; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(kFull, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
+template <class KeyT, class OrdT, class DistT, bool kSmem>
+__global__ void __launch_bounds__(kSortThreads, 1)
+    k_build_rows_ws(const int64_t* __restrict__ costs, int n, int m, int W, int Wp, int sitebits,
+                    int npasses, int dbits, OrdT* __restrict__ ord, DistT* __restrict__ dist,
+                    KeyT* __restrict__ gkeys) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);  // [warp][256]
+  uint32_t* tot = cnt + kWsWarps * 256;               // [256]
+  unsigned char* bufbase = smem + ((kWsWarps * 256 + 256 + 4) * 4 + 15) / 16 * 16;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  KeyT* A = kSmem ? reinterpret_cast<KeyT*>(bufbase) : gkeys + (size_t)blockIdx.x * 2 * m;
+  KeyT* B = A + m;
+  const unsigned lt = lanemask_lt();
+  const KeyT sitemask = (KeyT(1) << sitebits) - 1;
+  const unsigned dmask = (1u << dbits) - 1;
+  const int slice = (m + kWsWarps - 1) / kWsWarps;
+  const int s0 = min(m, warp * slice), s1 = min(m, s0 + slice);
+  uint32_t* mycnt = cnt + warp * 256;
+
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int64_t* crow = costs + (size_t)r * m;
+    for (int x = tid; x < m; x += kSortThreads) A[x] = ((KeyT)(uint64_t)crow[x] << sitebits) | (KeyT)x;
+    __syncthreads();
+    KeyT* src = A;
+    KeyT* dst = B;
+    for (int q = 0; q < npasses; ++q) {
+      const int shift = sitebits + q * dbits;
+      for (int d = lane; d < 256; d += 32) mycnt[d] = 0;
+      __syncwarp();
+      for (int x0 = s0; x0 < s1; x0 += 32) {
+        const int x = x0 + lane;
+        const bool valid = x < s1;
+        const unsigned d = valid ? (unsigned)(src[x] >> shift) & dmask : 0u;
+        const unsigned peers = digit_peers<8>(d, valid);
+        if (valid && (peers & lt) == 0) mycnt[d] += __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      if (tid < 256) {  // exclusive prefix over warps per digit; digit totals
+        uint32_t run = 0;
+        for (int w = 0; w < kWsWarps; ++w) {
+          const uint32_t c = cnt[w * 256 + tid];
+          cnt[w * 256 + tid] = run;
+          run += c;
+        }
+        tot[tid] = run;
+      }
+      __syncthreads();
+      const bool skip = tot[(unsigned)(src[0] >> shift) & dmask] == (uint32_t)m;  // constant digit
+      if (!skip) {
+        if (warp == 0) {  // exclusive scan of the digit totals, added into every warp's offsets
+          uint32_t v[8], s = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            v[j] = tot[lane * 8 + j];
+            s += v[j];
+          }
+          uint32_t incl = s;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+          }
+          uint32_t run = incl - s;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            tot[lane * 8 + j] = run;
+            run += v[j];
+          }
+        }
+        __syncthreads();
+        for (int d = lane; d < 256; d += 32) mycnt[d] += tot[d];
+        __syncwarp();
+        for (int x0 = s0; x0 < s1; x0 += 32) {
+          const int x = x0 + lane;
+          const bool valid = x < s1;
+          const KeyT key = valid ? src[x] : KeyT(0);
+          const unsigned d = valid ? (unsigned)(key >> shift) & dmask : 0u;
+          const unsigned peers = digit_peers<8>(d, valid);
+          const unsigned rank = __popc(peers & lt);
+          if (valid) dst[mycnt[d] + rank] = key;
+          __syncwarp();
+          if (valid && rank == 0) mycnt[d] += __popc(peers);
+          __syncwarp();
+        }
+        __syncthreads();
+        KeyT* t = src;
+        src = dst;
+        dst = t;
+      }
+    }
+    OrdT* orow = ord + (size_t)r * Wp;
+    DistT* drow = dist + (size_t)r * Wp;
+    for (int k = tid; k < Wp; k += kSortThreads) {
+      if (k < W) {
+        const KeyT key = src[k];
+        orow[k] = (OrdT)(uint32_t)(key & sitemask);
+        drow[k] = (DistT)(uint64_t)(key >> sitebits);
+      } else {
+        orow[k] = (OrdT)m;  // sentinel: T[m] == 0, never open
+        drow[k] = (DistT)0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- site-major narrow cost matrix for the gather-min kernel (K2b) --------
 
 // dT row stride nP = round_up(n, 16): 16-byte vector loads of consecutive
@@ -265,6 +398,24 @@ static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void
                                  void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st) {
   const size_t per = (size_t)bp.m * (sizeof(KeyT) + (kPayload ? 4 : 0)) * 2;
   const size_t smem = sort_smem_header() + per;
+  if constexpr (!kPayload) {  // packed keys: the warp-slice radix sort
+    const int dbits = 8;  // 8-bit digits, fully unrolled ballots (npasses = ceil(costbits / 8))
+    const size_t hs = sort_smem_header();
+    if (bp.smem_path) {
+      auto kern = k_build_rows_ws<KeyT, OrdT, DistT, true>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<bp.grid, kSortThreads, smem, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.npasses, dbits,
+                                                (OrdT*)ord, (DistT*)dist, nullptr);
+    } else {
+      auto kern = k_build_rows_ws<KeyT, OrdT, DistT, false>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
+      if (e != cudaSuccess) return e;
+      kern<<<bp.grid, kSortThreads, hs, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.npasses, dbits,
+                                              (OrdT*)ord, (DistT*)dist, (KeyT*)scratch_keys);
+    }
+    return cudaGetLastError();
+  }
   if (bp.smem_path) {
     auto kern = k_build_rows<KeyT, kPayload, OrdT, DistT, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,7 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
 exec > gpurun_out/timing.log 2>&1
-python tools/time_eval.py syn5k scan 10 "auto 64,12 64,10 64,8" 1
-python tools/time_eval.py sweep:100 scan 10 "auto 64,10 64,8 64,6" 1
-python tools/time_eval.py sweep:200 scan 10 "auto 64,10 64,8" 1
-python tools/time_eval.py pmed40 scan 10 "auto 64,16 64,12" 1
+timeout 900 python -m pytest tests -x -q -m gpu -k "parity or ingest" 2>&1 | tail -1
+python tools/prof_eval.py syn20k scan 1 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none -k regex:'k_build_rows' python tools/prof_eval.py syn20k scan 1 2>&1 | grep -E "gpu__time_duration|inst_exec" | head -4
