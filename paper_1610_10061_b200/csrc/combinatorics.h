@@ -20,6 +20,11 @@ class UBig {
     if (v) l_.push_back(v);
   }
   bool is_zero() const { return l_.empty(); }
+  size_t limbs() const { return l_.size(); }
+  // little-endian fixed-width export (L >= limbs())
+  void export_limbs(uint64_t* out, size_t L) const {
+    for (size_t i = 0; i < L; ++i) out[i] = i < l_.size() ? l_[i] : 0;
+  }
   int cmp(const UBig& o) const {
     if (l_.size() != o.l_.size()) return l_.size() < o.l_.size() ? -1 : 1;
     for (size_t i = l_.size(); i-- > 0;)
@@ -108,6 +113,29 @@ inline void unrank_combination(size_t m, size_t p, UBig r, uint64_t* words) {
     }
     ++candidate;
   }
+}
+
+// Pascal table C(a, k) for a < m, k < p as L-limb little-endian numbers,
+// entry (a * p + k) * L: with it, unranking needs only compares and
+// subtractions (the device unranking kernel in ga.cu).
+inline std::vector<uint64_t> binomial_table(size_t m, size_t p, size_t L) {
+  std::vector<uint64_t> t(m * p * L, 0);
+  for (size_t a = 0; a < m; ++a) {
+    t[(a * p + 0) * L] = 1;
+    if (a == 0) continue;
+    for (size_t k = 1; k < p; ++k) {
+      const uint64_t* x = &t[((a - 1) * p + k - 1) * L];
+      const uint64_t* y = &t[((a - 1) * p + k) * L];
+      uint64_t* z = &t[(a * p + k) * L];
+      unsigned __int128 carry = 0;
+      for (size_t i = 0; i < L; ++i) {
+        const unsigned __int128 s = (unsigned __int128)x[i] + y[i] + carry;
+        z[i] = (uint64_t)s;
+        carry = s >> 64;
+      }
+    }
+  }
+  return t;
 }
 
 // Uniform in [0, bound) from 64-bit draws with rejection (combinatorics.cpp:54-70).

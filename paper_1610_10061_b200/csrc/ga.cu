@@ -195,6 +195,49 @@ __global__ void k_popcount_check(const uint64_t* __restrict__ pop, int count, in
   if (pc != p) atomicMin(bad, (unsigned long long)idx);
 }
 
+// Reference-exact unranking on the device (combinatorics.cpp:20-52 with the
+// binomials read from a Pascal table instead of updated by multiply/divide):
+// walk the candidates, take candidate when C(a, k) > r, else r -= C(a, k).
+template <int kL>
+__global__ void k_unrank(const uint64_t* __restrict__ ranks, const uint64_t* __restrict__ table, int m, int p,
+                         int L, int wp, int count, uint64_t* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  uint64_t r[kL];
+#pragma unroll
+  for (int i = 0; i < kL; ++i) r[i] = i < L ? ranks[(size_t)idx * L + i] : 0;
+  uint64_t* w = out + (size_t)idx * wp;
+  for (int i = 0; i < wp; ++i) w[i] = 0;
+  int a = m - 1, k = p - 1, candidate = 0, remaining = p;
+  while (remaining > 0) {
+    const uint64_t* cur = table + ((size_t)a * p + k) * L;
+    int cmp = 0;  // sign of cur - r, most significant limb first
+    for (int i = L - 1; i >= 0 && cmp == 0; --i) {
+      const uint64_t x = __ldg(cur + i);
+      cmp = x > r[i] ? 1 : (x < r[i] ? -1 : 0);
+    }
+    if (cmp > 0) {
+      w[candidate >> 6] |= 1ull << (candidate & 63);
+      if (--remaining == 0) break;
+      --a;
+      --k;
+    } else {
+      uint64_t borrow = 0;
+#pragma unroll
+      for (int i = 0; i < kL; ++i) {
+        if (i < L) {
+          const uint64_t x = __ldg(cur + i);
+          const uint64_t d = r[i] - x - borrow;
+          borrow = (r[i] < x) || (r[i] - x < borrow);
+          r[i] = d;
+        }
+      }
+      --a;
+    }
+    ++candidate;
+  }
+}
+
 static unsigned cdiv(size_t a, unsigned b) { return (unsigned)((a + b - 1) / b); }
 
 // ---- GA engine ---------------------------------------------------------------------
@@ -311,12 +354,26 @@ struct HostDraw {
   Stream stream;
   UBig bound;
   size_t m = 0, p = 0;
+  size_t L = 0;                // limbs of the device table / ranks (0: host unranking)
+  std::vector<uint64_t> ranks;  // this rank's draws, count x L
   void init(uint64_t seed, size_t m_, size_t p_) {
     const uint64_t key[1] = {kHostTag};
     stream = Stream::derive(seed, key, 1);
     m = m_;
     p = p_;
     bound = binomial(m, p);
+    // the largest table entry is C(m-1, min(p-1, (m-1)/2)); ranks are < C(m, p)
+    const size_t L0 = std::max(binomial(m - 1, std::min(p - 1, (m - 1) / 2)).limbs(), bound.limbs()) + 1;
+    if (L0 <= 32 && m * p * L0 * 8 <= (size_t)256 << 20) L = L0;
+  }
+  // Draws every rank of the run's population (the stream is sequential over
+  // all islands) and keeps [lo, hi) as fixed-width limbs for the device.
+  void draw_ranks(size_t total, size_t lo, size_t hi) {
+    ranks.assign((hi - lo) * L, 0);
+    for (size_t i = 0; i < total; ++i) {
+      UBig r = random_below(bound, stream);
+      if (i >= lo && i < hi) r.export_limbs(&ranks[(i - lo) * L], L);
+    }
   }
   void draw(size_t total, size_t lo, size_t hi, uint64_t* out /* (hi-lo) x wp */) {
     std::vector<UBig> ranks;
@@ -418,8 +475,25 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     hd.init(cfg->seed, s.m, s.p);
     host_pop.resize(count * wp);
   }
+  if (ref_draw && hd.L) {  // the Pascal table for device unranking, once per run
+    const std::vector<uint64_t> tab = binomial_table(s.m, s.p, hd.L);
+    PM_CUDA_TRY(c, B.table.ensure(tab.size() * 8));
+    PM_CUDA_TRY(c, B.ranks.ensure(count * hd.L * 8));
+    PM_CUDA_TRY(c, cudaMemcpy(B.table.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+  }
   auto draw = [&](DevBuf& dst, uint64_t generation) -> int {
-    if (ref_draw) {
+    if (ref_draw && hd.L) {
+      hd.draw_ranks(nb * nt, block0 * nt, (block0 + nbl) * nt);
+      PM_CUDA_TRY(c, cudaMemcpyAsync(B.ranks.p, hd.ranks.data(), hd.ranks.size() * 8, cudaMemcpyHostToDevice,
+                                     c->stream));
+      const int L = (int)hd.L;
+      const unsigned g = cdiv(count, 128);
+      if (L <= 8) k_unrank<8><<<g, 128, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      else if (L <= 16) k_unrank<16><<<g, 128, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      else k_unrank<32><<<g, 128, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      PM_CUDA_TRY(c, cudaGetLastError());
+      c->launches += 1;
+    } else if (ref_draw) {
       hd.draw(nb * nt, block0 * nt, (block0 + nbl) * nt, host_pop.data());
       PM_CUDA_TRY(c, cudaMemcpyAsync(dst.p, host_pop.data(), count * wp * 8, cudaMemcpyHostToDevice, c->stream));
     } else {
