@@ -30,6 +30,9 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -144,13 +147,12 @@ struct MaskOps {
 // from global memory through L1/L2 (any m).
 //
 // Per chunk of 16 columns a lane (1) looks up the 16 masks, (2) walks them to
-// update `alive`, parking each column's newly-dead chromosomes h_j and the
-// column's cost in a per-lane shared-memory slot (predicated stores), and (3)
-// drains the parked hits in one loop whose trip count is the lane's hit count
-// for the whole chunk, into per-lane private counters acc[c][lane] (no
-// atomics, no bank conflicts).  Draining per chunk instead of per column keeps
-// the warp converged: the loop runs max_lane(hits in chunk) times, not
-// sum_j max_lane(hits in column j).
+// update `alive`, appending each column's newly-dead chromosomes h_j and the
+// column's cost to the warp's shared-memory queue (ballot + popc position, no
+// loops), and (3) the warp drains the queue lane-parallel into per-lane
+// private counters acc[c][lane] (no atomics, no bank conflicts).  The drain
+// loop runs the largest record's bit count, so one lane's burst of hits at a
+// client start no longer stalls the warp.
 template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kDepth>
 __global__ void __launch_bounds__(512, 1)
     k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
@@ -435,8 +437,19 @@ cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* 
                         int depth_mode, cudaStream_t st) {
   g_depth = depth_mode != 0;
   const void* fn = scan_kernel_ptr(t, sp.acc32, sp.G, sp.tsmem);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem);
-  if (e != cudaSuccess) return e;
+  // raise the kernel's dynamic shared-memory cap only when it grows (the call
+  // costs host time on every launch otherwise; the GA launches K2 ~10x per generation)
+  static thread_local std::vector<std::pair<const void*, size_t>> raised;
+  size_t* have = nullptr;
+  for (auto& f : raised)
+    if (f.first == fn) have = &f.second;
+  cudaError_t e = cudaSuccess;
+  if (!have || *have < sp.smem) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp.smem);
+    if (e != cudaSuccess) return e;
+    if (have) *have = sp.smem;
+    else raised.emplace_back(fn, sp.smem);
+  }
   const int groups = (int)((count + sp.G - 1) / sp.G);
   const int ctas = (int)std::min<long long>(sp.ctas, (long long)groups * t.n);
   size_t Ts = scan_t_stride(t.m);
