@@ -209,6 +209,18 @@ class RefLib:
         L.ref_parse.argtypes = [C.c_int, C.c_char_p, _i64p, _sz, C.POINTER(_sz), C.POINTER(_sz),
                                 C.POINTER(_sz)]
 
+    def run_benchmark(self, path, orlib=False, nb=60, nt=256, evolve_limit=100, saturation=10, seed=1,
+                      cx=-1, mu=-1, team=False, repeats=1, p_override=0, reference=-1, structured=True):
+        """The reference CLI pipeline (run_benchmark + emit_report) -> (rc, report text)."""
+        self.L.ref_run_benchmark.argtypes = [C.c_char_p, C.c_int, _sz, _sz, _sz, _sz, C.c_uint64,
+                                             C.c_longlong, C.c_longlong, C.c_int, _sz, _sz,
+                                             C.c_longlong, C.c_int, C.c_char_p, _sz]
+        buf = C.create_string_buffer(1 << 16)
+        rc = self.L.ref_run_benchmark(str(path).encode(), int(orlib), nb, nt, evolve_limit, saturation,
+                                      seed, cx, mu, int(team), repeats, p_override, reference,
+                                      int(structured), buf, len(buf))
+        return rc, buf.value.decode()
+
     def parse(self, text: str, orlib: bool = True, cap: int = 1 << 22):
         """parse_orlib / parse_dense -> (rc, n, m, p, costs)"""
         out = np.zeros(cap, dtype=np.int64)

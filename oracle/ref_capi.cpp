@@ -309,6 +309,25 @@ int ref_parse(int orlib, const char* text, std::int64_t* costs_out, std::size_t 
   });
 }
 
+// run_benchmark + emit_report (bench.cpp:230-323): the reference CLI's pipeline.
+int ref_run_benchmark(const char* path, int orlib, std::size_t nb, std::size_t nt, std::size_t evolve_limit,
+                      std::size_t saturation, std::uint64_t seed, long long cx, long long mu, int team,
+                      std::size_t repeats, std::size_t p_override, long long reference, int structured,
+                      char* out, std::size_t cap) {
+  return guard([&] {
+    const GaConfig cfg = make_cfg(nb, nt, evolve_limit, saturation, seed, cx, mu, team);
+    BenchOptions o;
+    o.repeats = repeats;
+    if (p_override) o.p_override = p_override;
+    std::optional<std::int64_t> ref;
+    if (reference >= 0) ref = reference;
+    const BenchmarkRecord r =
+        run_benchmark(path, orlib ? InstanceFormat::OrLib : InstanceFormat::Dense, cfg, ref, o);
+    const std::string s = emit_report({&r, 1}, structured ? ReportStyle::Structured : ReportStyle::Table);
+    std::snprintf(out, cap, "%s", s.c_str());
+  });
+}
+
 int ref_validate_config(std::size_t nb, std::size_t nt, std::size_t evolve_limit,
                         std::size_t saturation, int team) {
   return guard([&] { make_cfg(nb, nt, evolve_limit, saturation, 1, -1, -1, team).validate(); });

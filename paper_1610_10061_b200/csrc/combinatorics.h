@@ -7,6 +7,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "ga_ops.cuh"
@@ -66,6 +67,18 @@ class UBig {
     else if (v) l_.push_back(v);
   }
   size_t bit_length() const { return l_.empty() ? 0 : 64 * (l_.size() - 1) + (64 - __builtin_clzll(l_.back())); }
+  std::string str() const {  // decimal
+    if (l_.empty()) return "0";
+    UBig t = *this;
+    std::string out;
+    while (!t.is_zero()) {
+      const uint64_t r = t.div(10000000000000000000ULL);
+      std::string chunk = std::to_string(r);
+      if (!t.is_zero()) chunk.insert(0, 19 - chunk.size(), '0');
+      out.insert(0, chunk);
+    }
+    return out;
+  }
   void dec() {  // *this -= 1, requires *this >= 1
     for (auto& x : l_)
       if (x-- != 0) break;
