@@ -18,7 +18,9 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpmedian_b200.so")
+# PMB_LIBRARY: an alternative in-tree build of the same library (A/B kernel
+# experiments, tools/build_ab.sh); the default is the one `make` builds
+LIB_PATH = os.environ.get("PMB_LIBRARY") or os.path.join(_HERE, "libpmedian_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

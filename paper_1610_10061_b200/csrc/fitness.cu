@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         qn += __popc(hb);
       }
+      __syncwarp();  // queue writes visible to the draining lanes
       // drain: lane r applies queue records r, r+32, ... -- the loop runs the
       // largest record's bit count, not the busiest lane's hit count
       for (uint32_t base = 0; base < qn; base += 32) {
@@ -311,6 +312,7 @@ __global__ void __launch_bounds__(512, 1)
           myacc[c * 32] += dv;
         }
       }
+      __syncwarp();  // the next step rewrites the queue
       if (i >= 0) {
         k += kChunk;
         if (alive == 0 || k >= Wp) {
