@@ -128,26 +128,28 @@ inline void unrank_combination(size_t m, size_t p, UBig r, uint64_t* words) {
   }
 }
 
-// Pascal table C(a, k) for a < m, k < p as L-limb little-endian numbers,
-// entry (a * p + k) * L: with it, unranking needs only compares and
-// subtractions (the device unranking kernel in ga.cu).
+// Pascal table for the device unranking kernel: C(x, y) for y <= p, x < m as
+// L-limb little-endian numbers, entry (y * m + x) * L (consecutive x adjacent,
+// so a warp testing 32 consecutive candidates reads one contiguous run),
+// followed by C(m, p) itself.
 inline std::vector<uint64_t> binomial_table(size_t m, size_t p, size_t L) {
-  std::vector<uint64_t> t(m * p * L, 0);
-  for (size_t a = 0; a < m; ++a) {
-    t[(a * p + 0) * L] = 1;
-    if (a == 0) continue;
-    for (size_t k = 1; k < p; ++k) {
-      const uint64_t* x = &t[((a - 1) * p + k - 1) * L];
-      const uint64_t* y = &t[((a - 1) * p + k) * L];
-      uint64_t* z = &t[(a * p + k) * L];
+  std::vector<uint64_t> t(((p + 1) * m + 1) * L, 0);
+  auto at = [&](size_t x, size_t y) { return &t[(y * m + x) * L]; };
+  for (size_t x = 0; x < m; ++x) at(x, 0)[0] = 1;
+  for (size_t y = 1; y <= p; ++y) {
+    for (size_t x = 1; x < m; ++x) {  // C(x, y) = C(x-1, y-1) + C(x-1, y); C(0, y) = 0
+      const uint64_t* a = at(x - 1, y - 1);
+      const uint64_t* b = at(x - 1, y);
+      uint64_t* z = at(x, y);
       unsigned __int128 carry = 0;
       for (size_t i = 0; i < L; ++i) {
-        const unsigned __int128 s = (unsigned __int128)x[i] + y[i] + carry;
+        const unsigned __int128 s = (unsigned __int128)a[i] + b[i] + carry;
         z[i] = (uint64_t)s;
         carry = s >> 64;
       }
     }
   }
+  binomial(m, p).export_limbs(&t[(p + 1) * m * L], L);
   return t;
 }
 

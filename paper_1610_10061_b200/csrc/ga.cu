@@ -31,6 +31,7 @@
 
 #include "combinatorics.h"
 #include "ctx.h"
+#include "common.cuh"
 #include "ga_ops.cuh"
 
 namespace pmb {
@@ -195,47 +196,88 @@ __global__ void k_popcount_check(const uint64_t* __restrict__ pop, int count, in
   if (pc != p) atomicMin(bad, (unsigned long long)idx);
 }
 
-// Reference-exact unranking on the device (combinatorics.cpp:20-52 with the
-// binomials read from a Pascal table instead of updated by multiply/divide):
-// walk the candidates, take candidate when C(a, k) > r, else r -= C(a, k).
+// Reference-exact unranking on the device (combinatorics.cpp:20-52): the
+// rank-th p-subset of {0..m-1} in lexicographic order.  The reference walks
+// the candidates one by one (take candidate when C(a, k) > r, else
+// r -= C(a, k)); a run of skips telescopes (hockey stick:
+// sum_{t<j} C(a-t, k) = C(a+1, k+1) - C(a-j+1, k+1)), so with X = C(a+1, k+1) - r
+// the next taken candidate is the first j with C(a-j, k+1) < X, after which
+// X -= C(a-j, k+1), a -= j+1, k -= 1.  One warp per chromosome tests 32
+// consecutive candidates per probe (one contiguous table run), so a draw costs
+// ~p dependent probes instead of ~m.  Same subsets as the reference's walk,
+// bit for bit (tests/test_gpu_ga.py).
 template <int kL>
-__global__ void k_unrank(const uint64_t* __restrict__ ranks, const uint64_t* __restrict__ table, int m, int p,
-                         int L, int wp, int count, uint64_t* __restrict__ out) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= count) return;
-  uint64_t r[kL];
+__global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ranks,
+                                                const uint64_t* __restrict__ table, int m, int p, int L, int wp,
+                                                int count, uint64_t* __restrict__ out) {
+  const int idx = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (idx >= count) return;  // warp-uniform
+  const uint64_t* bound = table + (size_t)(p + 1) * m * L;
+  uint64_t X[kL];  // X = C(m, p) - r (every lane holds the same value)
+  {
+    uint64_t borrow = 0;
 #pragma unroll
-  for (int i = 0; i < kL; ++i) r[i] = i < L ? ranks[(size_t)idx * L + i] : 0;
-  uint64_t* w = out + (size_t)idx * wp;
-  for (int i = 0; i < wp; ++i) w[i] = 0;
-  int a = m - 1, k = p - 1, candidate = 0, remaining = p;
-  while (remaining > 0) {
-    const uint64_t* cur = table + ((size_t)a * p + k) * L;
-    int cmp = 0;  // sign of cur - r, most significant limb first
-    for (int i = L - 1; i >= 0 && cmp == 0; --i) {
-      const uint64_t x = __ldg(cur + i);
-      cmp = x > r[i] ? 1 : (x < r[i] ? -1 : 0);
-    }
-    if (cmp > 0) {
-      w[candidate >> 6] |= 1ull << (candidate & 63);
-      if (--remaining == 0) break;
-      --a;
-      --k;
-    } else {
-      uint64_t borrow = 0;
-#pragma unroll
-      for (int i = 0; i < kL; ++i) {
-        if (i < L) {
-          const uint64_t x = __ldg(cur + i);
-          const uint64_t d = r[i] - x - borrow;
-          borrow = (r[i] < x) || (r[i] - x < borrow);
-          r[i] = d;
-        }
+    for (int i = 0; i < kL; ++i) {
+      if (i < L) {
+        const uint64_t b = __ldg(bound + i), r = __ldg(ranks + (size_t)idx * L + i);
+        X[i] = b - r - borrow;
+        borrow = (b < r) || (b - r < borrow);
+      } else {
+        X[i] = 0;
       }
-      --a;
     }
-    ++candidate;
   }
+  uint64_t* w = out + (size_t)idx * wp;
+  for (int i = lane; i < wp; i += 32) w[i] = 0;
+  __syncwarp();
+  int a = m - 1, k = p - 1, base = 0;
+  int word_idx = 0;
+  uint64_t word = 0;  // the output word being filled (candidates increase)
+  while (k >= 0) {
+    const int x = a - base - lane;
+    uint64_t cv[kL];
+    int cmp = -1;  // sign of C(x, k+1) - X; C(x, .) = 0 for x < 0
+    if (x >= 0) {
+      const uint64_t* cp = table + ((size_t)(k + 1) * m + x) * L;
+#pragma unroll
+      for (int i = 0; i < kL; ++i) cv[i] = i < L ? __ldg(cp + i) : 0;
+      cmp = 0;
+#pragma unroll
+      for (int i = kL - 1; i >= 0; --i)
+        if (cmp == 0 && i < L) cmp = cv[i] < X[i] ? -1 : (cv[i] > X[i] ? 1 : 0);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kL; ++i) cv[i] = 0;
+    }
+    const unsigned hit = __ballot_sync(kFull, cmp < 0);
+    if (!hit) {
+      base += 32;
+      continue;
+    }
+    const int jl = __ffs(hit) - 1, j = base + jl;
+    uint64_t borrow = 0;  // X -= C(a - j, k + 1), the limbs from lane jl
+#pragma unroll
+    for (int i = 0; i < kL; ++i) {
+      if (i < L) {
+        const uint64_t v = __shfl_sync(kFull, cv[i], jl);
+        const uint64_t d = X[i] - v - borrow;
+        borrow = (X[i] < v) || (X[i] - v < borrow);
+        X[i] = d;
+      }
+    }
+    const int cand = m - 1 - a + j;
+    if ((cand >> 6) != word_idx) {
+      if (lane == 0 && word) w[word_idx] = word;
+      word_idx = cand >> 6;
+      word = 0;
+    }
+    word |= 1ull << (cand & 63);
+    a -= j + 1;
+    --k;
+    base = 0;
+  }
+  if (lane == 0 && word) w[word_idx] = word;
 }
 
 static unsigned cdiv(size_t a, unsigned b) { return (unsigned)((a + b - 1) / b); }
@@ -362,9 +404,10 @@ struct HostDraw {
     m = m_;
     p = p_;
     bound = binomial(m, p);
-    // the largest table entry is C(m-1, min(p-1, (m-1)/2)); ranks are < C(m, p)
-    const size_t L0 = std::max(binomial(m - 1, std::min(p - 1, (m - 1) / 2)).limbs(), bound.limbs()) + 1;
-    if (L0 <= 32 && m * p * L0 * 8 <= (size_t)256 << 20) L = L0;
+    // table entries C(x, y), x < m, y <= p, are at most C(m-1, min(p, (m-1)/2));
+    // ranks are < C(m, p)
+    const size_t L0 = std::max(binomial(m - 1, std::min(p, (m - 1) / 2)).limbs(), bound.limbs()) + 1;
+    if (L0 <= 32 && (m * (p + 1) + 1) * L0 * 8 <= (size_t)256 << 20) L = L0;
   }
   // Draws every rank of the run's population (the stream is sequential over
   // all islands) and keeps [lo, hi) as fixed-width limbs for the device.
@@ -487,10 +530,10 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
       PM_CUDA_TRY(c, cudaMemcpyAsync(B.ranks.p, hd.ranks.data(), hd.ranks.size() * 8, cudaMemcpyHostToDevice,
                                      c->stream));
       const int L = (int)hd.L;
-      const unsigned g = cdiv(count, 128);
-      if (L <= 8) k_unrank<8><<<g, 128, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
-      else if (L <= 16) k_unrank<16><<<g, 128, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
-      else k_unrank<32><<<g, 128, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      const unsigned g = cdiv(count * 32, 256);
+      if (L <= 8) k_unrank<8><<<g, 256, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      else if (L <= 16) k_unrank<16><<<g, 256, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      else k_unrank<32><<<g, 256, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 1;
     } else if (ref_draw) {

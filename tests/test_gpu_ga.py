@@ -159,3 +159,17 @@ def test_run_ga_device_population(ctx, pm, oracle):
     _cmp_run(a, b)
     assert sum(bin(int(x)).count("1") for x in a["best"]) == 20
     assert oracle.direct_cost(200, 200, 20, costs, a["best"]) == (0, a["best_cost"])
+
+
+@pytest.mark.parametrize("npts,p", [(1500, 150), (2200, 330), (2600, 520)])
+def test_run_ga_wide_ranks_match_reference(ctx, pm, oracle, reflib, npts, p):
+    """Population draws whose ranks need 12 / 22 limbs (the device unranking's
+    16- and 32-limb kernels) and 31 limbs (Pascal table over 256 MB: host
+    unranking), against the reference's own draw."""
+    costs = oracle.synth_euclid(npts)
+    ctx.set_instance(costs, npts, npts, p)
+    ri = reflib.create(npts, npts, p, costs)
+    got = ctx.run_ga(pm.ga_config(nb=2, nt=8, evolve_limit=2, saturation=5, seed=4))
+    rc, want = ri.run_ga(2, 8, 2, 5, 4, workers=16)
+    assert rc == 0
+    _cmp_run(got, want)
