@@ -154,6 +154,17 @@ def barrier(world):
         dist.barrier()
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_reference_sample(site_order, increments, n, m, p, words, gpu_costs, budget_s=10.0):
     """The reference's own fitness() (oracle/_ref, compiled from /root/reference sources)
     on all host threads over a bounded sample of the same population."""
@@ -175,10 +186,15 @@ def cpu_reference_sample(site_order, increments, n, m, p, words, gpu_costs, budg
     rc, costs, _ = ri.evaluate(sample, threads)
     dt = time.perf_counter() - t0
     parity = bool(rc == 0 and (costs == gpu_costs[:count]).all())
+    # one worker too, ~2 s of work
+    one = int(max(1, min(count, 2.0 / max(per_eval, 1e-9))))
+    t0 = time.perf_counter()
+    ri.evaluate(words[:one], 1)
+    dt1 = time.perf_counter() - t0
     return {"value": count / dt, "unit": "evals/s", "cores": threads, "kind": "reference",
             "sample": f"first {count} chromosomes of the same population, reference fitness() "
                       f"(proj/src/ordering.cpp:40-59) on {threads} host threads, {dt:.1f} s",
-            "bit_exact_vs_gpu": parity}
+            "bit_exact_vs_gpu": parity, "single_thread_value": one / dt1, "cpu_model": cpu_model()}
 
 
 def run_ours(args):
@@ -369,8 +385,44 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
                 "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
                 "best_cost": r["best_cost"],
                 "evals_per_gen_reference_semantics": r["evaluations"] / r["kernels_executed"]}
+        # full runs at the paper's Table-1 settings (evolve_limit=100, saturation=10,
+        # acceptance.cpp:323-328), reference-exact population draw
+        full = pm.ga_config(nb=60, nt=256, evolve_limit=100, saturation=10, seed=1)
+        r = c2.run_ga(full)
+        out["pmed40_shape_full_run"] = {
+            "config": "synthetic Euclidean n=m=900, p=90, nb=60, nt=256, evolve_limit=100, saturation=10, seed 1",
+            "generations": r["kernels_executed"], "kernel_of_best": r["kernel_of_best"],
+            "best_cost": r["best_cost"], "wall_s": r["wall_time"]}
         c2.close()
+        c3 = pm2.Context(local)
+        c3.set_instance(synth.euclid_costs(100, 12345), 100, 100, 5)
+        opt, nsub, t_ex = exhaustive_optimum(c3, 100, 5)
+        r = c3.run_ga(full)
+        out["pmed1_shape_full_run"] = {
+            "config": "synthetic Euclidean n=m=100, p=5, nb=60, nt=256, evolve_limit=100, saturation=10, seed 1",
+            "generations": r["kernels_executed"], "kernel_of_best": r["kernel_of_best"],
+            "best_cost": r["best_cost"], "wall_s": r["wall_time"], "optimum": opt,
+            "optimal": r["best_cost"] == opt,
+            "optimum_by": f"device evaluation of all {nsub} p-subsets ({t_ex:.1f} s incl. host enumeration)"}
+        c3.close()
     return out
+
+
+def exhaustive_optimum(ctx, m, p):
+    """min over every p-subset of range(m), each evaluated by the device path."""
+    import torch
+
+    from paper_1610_10061_b200 import synth
+    t0 = time.perf_counter()
+    best, total = None, 0
+    for chunk in synth.all_subsets(m, p):
+        w = torch.from_numpy(chunk.view(np.int64)).cuda()
+        out = torch.empty(chunk.shape[0], dtype=torch.int64, device="cuda")
+        ctx.evaluate_device(w, out, chunk.shape[0], chunk.shape[1], check=True)
+        v = int(out.min().item())
+        best = v if best is None else min(best, v)
+        total += chunk.shape[0]
+    return best, total, time.perf_counter() - t0
 
 
 def run_reference(args):
@@ -428,6 +480,14 @@ def run_reference(args):
                       f"{threads} worker threads",
             "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
             "best_cost": r["best_cost"]}}
+        # a full Table-1 run on the pmed1 shape (the 900/90 one would take minutes here)
+        ri = ref.create(100, 100, 5, synth.euclid_costs(100, 12345))
+        rc, r = ri.run_ga(60, 256, 100, 10, 1, workers=threads)
+        line["ga"]["pmed1_shape_full_run"] = {
+            "config": "synthetic Euclidean n=m=100, p=5, nb=60, nt=256, evolve_limit=100, saturation=10, seed 1; "
+                      f"reference run_ga, {threads} worker threads",
+            "generations": r["kernels_executed"], "kernel_of_best": r["kernel_of_best"],
+            "best_cost": r["best_cost"], "wall_s": r["wall_time"]}
     print(json.dumps(line), flush=True)
 
 

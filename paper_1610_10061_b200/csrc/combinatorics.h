@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstddef>
+#include <cmath>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -78,6 +79,17 @@ class UBig {
       out.insert(0, chunk);
     }
     return out;
+  }
+  double div_pow2(size_t bits) const {  // value / 2^bits, from the top two limbs
+    if (l_.empty()) return 0.0;
+    const size_t n = l_.size();
+    double mant = (double)l_[n - 1];
+    int e = 64 * (int)(n - 1);
+    if (n >= 2) {
+      mant = mant * 18446744073709551616.0 + (double)l_[n - 2];
+      e -= 64;
+    }
+    return std::ldexp(mant, e - (int)bits);
   }
   void dec() {  // *this -= 1, requires *this >= 1
     for (auto& x : l_)

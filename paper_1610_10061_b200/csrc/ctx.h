@@ -51,7 +51,7 @@ using pmb::BuildPlan;
 namespace pmb {
 // GA working set (ga.cu), grow-only and kept across calls.
 struct GaBuffers {
-  DevBuf pop, next, cost, before, child, ccost, ok, bcost, bthread, bwords, evals, tmp, table, ranks;
+  DevBuf pop, next, cost, before, child, ccost, ok, bcost, bthread, bwords, evals, tmp, table, ranks, rflags, rstate;
 };
 }  // namespace pmb
 using pmb::GaBuffers;

@@ -280,6 +280,88 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
   if (lane == 0 && word) w[word_idx] = word;
 }
 
+// Reference-exact rank draws on the device.  The reference draws every rank of
+// a generation's population from one sequential host stream (ga.cpp:226-235)
+// with random_below(C(m, p)) (combinatorics.cpp:54-70): an attempt consumes
+// `words` outputs (the first one masked to the top limb's bits, then shifted
+// in below) and is accepted when the value is below the bound.  Splitmix
+// outputs are random-access -- output i is mix64(state0 + (i+1) * gamma) -- so
+// every attempt of a generation is tested at once and the accepted ones are
+// compacted in stream order; the stream position lives on the device
+// (rstate[0]), so no host work and no synchronisation are involved.
+__device__ __forceinline__ void attempt_value(uint64_t state0, uint64_t first, int words, uint64_t top_mask,
+                                              uint64_t* v /* little-endian, words limbs */) {
+  for (int w = 0; w < words; ++w) {
+    uint64_t x = mix64(state0 + (first + (uint64_t)w + 1) * 0x9e3779b97f4a7c15ULL);
+    if (w == 0) x &= top_mask;
+    v[words - 1 - w] = x;
+  }
+}
+
+__global__ void k_rank_flags(uint64_t state0, const unsigned long long* __restrict__ rstate, int words,
+                             uint64_t top_mask, const uint64_t* __restrict__ bound, int L, int A,
+                             uint32_t* __restrict__ flags) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  uint64_t v[32];
+  attempt_value(state0, rstate[0] + (uint64_t)a * words, words, top_mask, v);
+  int cmp = 0;  // sign of v - bound, most significant limb first
+  for (int i = L - 1; i >= 0 && cmp == 0; --i) {
+    const uint64_t x = i < words ? v[i] : 0, b = bound[i];
+    cmp = x < b ? -1 : (x > b ? 1 : 0);
+  }
+  flags[a] = cmp < 0;
+}
+
+// One block: stream-order compaction of the accepted attempts; ranks [lo, hi)
+// of the population are written (islands keep their own slice), and the
+// stream position advances past the total-th accepted attempt.
+__global__ void __launch_bounds__(1024) k_rank_compact(uint64_t state0, unsigned long long* __restrict__ rstate,
+                                                       int words, uint64_t top_mask, int L, int A,
+                                                       const uint32_t* __restrict__ flags, int total, int lo,
+                                                       int hi, uint64_t* __restrict__ ranks) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t grand;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t pos = rstate[0];
+  const int seg = (A + blockDim.x - 1) / blockDim.x;
+  const int a0 = min(A, tid * seg), a1 = min(A, a0 + seg);
+  uint32_t cnt = 0;
+  for (int a = a0; a < a1; ++a) cnt += flags[a];
+  uint32_t incl = cnt;  // block exclusive scan of the per-thread counts
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t x = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0, xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, xi, o);
+      if (lane >= o) xi += t;
+    }
+    wsum[lane] = xi - x;
+    if (lane == 31) grand = xi;
+  }
+  __syncthreads();
+  uint32_t k = wsum[warp] + incl - cnt;
+  for (int a = a0; a < a1 && (int)k < total; ++a) {
+    if (!flags[a]) continue;
+    if ((int)k >= lo && (int)k < hi) {
+      uint64_t v[32];
+      attempt_value(state0, pos + (uint64_t)a * words, words, top_mask, v);
+      uint64_t* dst = ranks + (size_t)(k - lo) * L;
+      for (int i = 0; i < L; ++i) dst[i] = i < words ? v[i] : 0;
+    }
+    if ((int)k == total - 1) rstate[0] = pos + (uint64_t)(a + 1) * words;
+    ++k;
+  }
+  if (tid == 0 && grand < (uint32_t)total) rstate[1] = 1;  // window exhausted (checked by the host)
+}
+
 static unsigned cdiv(size_t a, unsigned b) { return (unsigned)((a + b - 1) / b); }
 
 // ---- GA engine ---------------------------------------------------------------------
@@ -396,27 +478,27 @@ struct HostDraw {
   Stream stream;
   UBig bound;
   size_t m = 0, p = 0;
-  size_t L = 0;                // limbs of the device table / ranks (0: host unranking)
-  std::vector<uint64_t> ranks;  // this rank's draws, count x L
+  size_t L = 0;                // limbs of the device table / ranks (0: host draw and unranking)
+  int words = 0;           // 64-bit outputs per random_below attempt
+  uint64_t top_mask = 0;   // mask of the first (most significant) output
+  double accept = 1.0;     // P(attempt accepted) = bound / 2^bits
   void init(uint64_t seed, size_t m_, size_t p_) {
     const uint64_t key[1] = {kHostTag};
     stream = Stream::derive(seed, key, 1);
     m = m_;
     p = p_;
     bound = binomial(m, p);
+    UBig bm1 = bound;
+    bm1.dec();
+    const size_t bits = bm1.bit_length();
+    words = (int)((bits + 63) / 64);
+    const size_t top = bits - 64 * (words - 1);
+    top_mask = top == 64 ? ~0ull : ((1ull << top) - 1);
+    accept = bound.div_pow2(bits);
     // table entries C(x, y), x < m, y <= p, are at most C(m-1, min(p, (m-1)/2));
     // ranks are < C(m, p)
     const size_t L0 = std::max(binomial(m - 1, std::min(p, (m - 1) / 2)).limbs(), bound.limbs()) + 1;
     if (L0 <= 32 && (m * (p + 1) + 1) * L0 * 8 <= (size_t)256 << 20) L = L0;
-  }
-  // Draws every rank of the run's population (the stream is sequential over
-  // all islands) and keeps [lo, hi) as fixed-width limbs for the device.
-  void draw_ranks(size_t total, size_t lo, size_t hi) {
-    ranks.assign((hi - lo) * L, 0);
-    for (size_t i = 0; i < total; ++i) {
-      UBig r = random_below(bound, stream);
-      if (i >= lo && i < hi) r.export_limbs(&ranks[(i - lo) * L], L);
-    }
   }
   void draw(size_t total, size_t lo, size_t hi, uint64_t* out /* (hi-lo) x wp */) {
     std::vector<UBig> ranks;
@@ -523,13 +605,26 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     PM_CUDA_TRY(c, B.table.ensure(tab.size() * 8));
     PM_CUDA_TRY(c, B.ranks.ensure(count * hd.L * 8));
     PM_CUDA_TRY(c, cudaMemcpy(B.table.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+    PM_CUDA_TRY(c, B.rstate.ensure(16));  // {stream position, window-exhausted flag}
+    PM_CUDA_TRY(c, cudaMemsetAsync(B.rstate.p, 0, 16, c->stream));
   }
   auto draw = [&](DevBuf& dst, uint64_t generation) -> int {
     if (ref_draw && hd.L) {
-      hd.draw_ranks(nb * nt, block0 * nt, (block0 + nbl) * nt);
-      PM_CUDA_TRY(c, cudaMemcpyAsync(B.ranks.p, hd.ranks.data(), hd.ranks.size() * 8, cudaMemcpyHostToDevice,
-                                     c->stream));
-      const int L = (int)hd.L;
+      const int L = (int)hd.L, total = (int)(nb * nt);
+      // attempts window: the accepted count falls short of `total` with
+      // probability < 1e-30 (12 sigma); a shortfall is reported, never ignored
+      const int A = (int)std::ceil((total + 12.0 * std::sqrt((double)total) + 64.0) / hd.accept);
+      PM_CUDA_TRY(c, B.rflags.ensure((size_t)A * 4));
+      const uint64_t* bound = B.table.as<uint64_t>() + (size_t)(s.p + 1) * s.m * L;
+      k_rank_flags<<<cdiv(A, 256), 256, 0, c->stream>>>(hd.stream.state, B.rstate.as<unsigned long long>(),
+                                                       hd.words, hd.top_mask, bound, L, A,
+                                                       B.rflags.as<uint32_t>());
+      k_rank_compact<<<1, 1024, 0, c->stream>>>(hd.stream.state, B.rstate.as<unsigned long long>(), hd.words,
+                                                hd.top_mask, L, A, B.rflags.as<uint32_t>(), total,
+                                                (int)(block0 * nt), (int)((block0 + nbl) * nt),
+                                                B.ranks.as<uint64_t>());
+      PM_CUDA_TRY(c, cudaGetLastError());
+      c->launches += 2;
       const unsigned g = cdiv(count * 32, 256);
       if (L <= 8) k_unrank<8><<<g, 256, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
       else if (L <= 16) k_unrank<16><<<g, 256, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
@@ -616,9 +711,12 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     }
     std::swap(B.pop, B.next);
   }
-  unsigned long long ref_evals = 0;
+  unsigned long long ref_evals = 0, rstate[2] = {0, 0};
   PM_CUDA_TRY(c, cudaMemcpyAsync(&ref_evals, B.evals.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  if (ref_draw && hd.L)
+    PM_CUDA_TRY(c, cudaMemcpyAsync(rstate, B.rstate.p, 16, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (rstate[1]) return c->fail(PM_CUDA, "population draw: attempt window exhausted");
   size_t fb = 0;
   rc = pm_check_errors(c, &fb);
   if (rc) return rc;

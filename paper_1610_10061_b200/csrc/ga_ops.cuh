@@ -111,42 +111,48 @@ __device__ void random_shift_mutation(const uint64_t* in, uint64_t* out, int m, 
   rotate_range(in, out, m, lo, len, offset);
 }
 
+// The lowest k set bits of x (all of x when it has at most k).
+__device__ __forceinline__ uint64_t lowest_bits(uint64_t x, int k) {
+  if (k <= 0) return 0;
+  for (int n = __popcll(x); n > k; --n) x ^= 1ull << (63 - __clzll((long long)x));
+  return x;
+}
+
 // crossover (ga.cpp:35-63): child starts as a; scanning cyclically from
 // `start`, differing positions adopt b's gene while the closed->open and
-// open->closed quotas (exchanges/2 each) last.  Returns success.
+// open->closed quotas (exchanges/2 each) last; success iff both quotas are
+// used up.  Word-level: the scan visits words start>>6 .. wp-1, then
+// 0 .. start>>6 (wp + 1 steps, the start word split in two), taking the
+// lowest still-allowed differing bits of each class; a single loop with no
+// early exit (an earlier nested-loop form with a mid-loop return was
+// observed to run differently from its source on sm_100a in some processes).
 __device__ bool crossover(const uint64_t* a, const uint64_t* b, uint64_t* child, int m, int start,
                           int exchanges) {
-  const int wp = (m + 63) >> 6;
+  const int wp = (m + 63) >> 6, sw = start >> 6;
   for (int wi = 0; wi < wp; ++wi) child[wi] = a[wi];
   int oq = exchanges / 2, cq = exchanges / 2;
-  // two segments: [start, m) then [0, start)
-  for (int seg = 0; seg < 2; ++seg) {
-    const int s0 = seg == 0 ? start : 0, s1 = seg == 0 ? m : start;
-    for (int wi = s0 >> 6; s0 < s1 && wi <= ((s1 - 1) >> 6); ++wi) {
-      uint64_t range = ~0ull;
-      if (wi == (s0 >> 6)) range &= ~0ull << (s0 & 63);
-      if (wi == ((s1 - 1) >> 6)) range &= low_mask(((s1 - 1) & 63) + 1);
-      const uint64_t diff = (a[wi] ^ b[wi]) & range;
-      uint64_t opn = diff & ~a[wi], cls = diff & a[wi];
-      // the position where the later quota runs out ends the scan
-      uint64_t take_o = 0, take_c = 0;
-      while (opn && oq > 0) {
-        const uint64_t lb = opn & (0 - opn);
-        take_o |= lb;
-        opn ^= lb;
-        --oq;
-      }
-      while (cls && cq > 0) {
-        const uint64_t lb = cls & (0 - cls);
-        take_c |= lb;
-        cls ^= lb;
-        --cq;
-      }
-      child[wi] = (child[wi] | take_o) & ~take_c;
-      if (oq == 0 && cq == 0) return true;
+  bool done = oq == 0 && cq == 0;
+  for (int step = 0; step <= wp; ++step) {
+    if (done) break;
+    const bool first = step < wp - sw;  // [start, m) first, then [0, start)
+    const int wi = first ? sw + step : step - (wp - sw);
+    uint64_t range = ~0ull;
+    if (first) {
+      if (wi == sw) range &= ~0ull << (start & 63);
+      if (wi == wp - 1) range &= low_mask(((m - 1) & 63) + 1);
+    } else if (wi == sw) {
+      range &= low_mask(start & 63);
     }
+    const uint64_t aw = a[wi];
+    const uint64_t diff = (aw ^ b[wi]) & range;
+    const uint64_t take_o = lowest_bits(diff & ~aw, oq);
+    const uint64_t take_c = lowest_bits(diff & aw, cq);
+    oq -= __popcll(take_o);
+    cq -= __popcll(take_c);
+    child[wi] = (child[wi] | take_o) & ~take_c;
+    done = oq == 0 && cq == 0;
   }
-  return false;
+  return done;
 }
 
 __host__ __device__ __forceinline__ uint32_t crossover_couple(uint32_t t, uint32_t round, uint32_t nt) {

@@ -150,3 +150,41 @@ def random_population(m: int, p: int, count: int, seed: int = 7) -> np.ndarray:
         sites = np.fromiter((perm.get(j, j) for j in range(p)), dtype=np.int64, count=p)
         np.bitwise_or.at(words[c], sites >> 6, np.left_shift(np.uint64(1), (sites & 63).astype(np.uint64)))
     return words
+
+
+def _subsets(m: int, k: int):
+    """All k-subsets of range(m) as (words [N, wp] u64, min, max); k small."""
+    import itertools
+    wp = (m + 63) // 64
+    comb = np.array(list(itertools.combinations(range(m), k)), dtype=np.int64).reshape(-1, k)
+    words = np.zeros((comb.shape[0], wp), dtype=np.uint64)
+    for c in range(k):
+        np.bitwise_or.at(words, (np.arange(comb.shape[0]), comb[:, c] >> 6),
+                         np.left_shift(np.uint64(1), (comb[:, c] & 63).astype(np.uint64)))
+    lo = comb[:, 0] if k else np.full(1, m, dtype=np.int64)
+    hi = comb[:, -1] if k else np.full(1, -1, dtype=np.int64)
+    return words, lo, hi
+
+
+def all_subsets(m: int, p: int, chunk: int = 1 << 22):
+    """Every p-subset of range(m) exactly once, as chunks of chromosome words
+    (exhaustive optima for small instances, e.g. the pmed1 shape C(100, 5)).
+    A p-subset = a (p//2)-subset followed by a (p - p//2)-subset whose
+    minimum exceeds the first part's maximum."""
+    a_words, _, a_hi = _subsets(m, p // 2)
+    b_words, b_lo, _ = _subsets(m, p - p // 2)
+    order = np.argsort(b_lo, kind="stable")
+    b_words, b_lo = b_words[order], b_lo[order]
+    buf, size = [], 0
+    for i in range(a_words.shape[0]):
+        j = int(np.searchsorted(b_lo, a_hi[i] + 1))
+        if j == b_words.shape[0]:
+            continue
+        part = b_words[j:] | a_words[i]
+        buf.append(part)
+        size += part.shape[0]
+        if size >= chunk:
+            yield np.concatenate(buf)
+            buf, size = [], 0
+    if buf:
+        yield np.concatenate(buf)

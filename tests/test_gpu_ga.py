@@ -173,3 +173,47 @@ def test_run_ga_wide_ranks_match_reference(ctx, pm, oracle, reflib, npts, p):
     rc, want = ri.run_ga(2, 8, 2, 5, 4, workers=16)
     assert rc == 0
     _cmp_run(got, want)
+
+
+def test_full_run_pmed1_shape_reaches_exhaustive_optimum(ctx, pm, reflib):
+    """BASELINE config 1 on a synthetic pmed1-shaped instance (n=m=100, p=5; the
+    OR-Library files are absent): the paper's Table-1 run (nb=60, nt=256,
+    evolve_limit=100, saturation=10) gives the reference's RunResult and the
+    optimum, found by evaluating all C(100, 5) = 75,287,520 subsets on the device."""
+    import torch
+
+    from paper_1610_10061_b200 import synth
+    costs = synth.euclid_costs(100, 12345)
+    ctx.set_instance(costs, 100, 100, 5)
+    best = None
+    for chunk in synth.all_subsets(100, 5):
+        w = torch.from_numpy(chunk.view(np.int64)).cuda()
+        out = torch.empty(chunk.shape[0], dtype=torch.int64, device="cuda")
+        ctx.evaluate_device(w, out, chunk.shape[0], chunk.shape[1], check=True)
+        v = int(out.min().item())
+        best = v if best is None else min(best, v)
+    got = ctx.run_ga(pm.ga_config(nb=60, nt=256, evolve_limit=100, saturation=10, seed=1))
+    rc, want = reflib.create(100, 100, 5, costs).run_ga(60, 256, 100, 10, 1, workers=16)
+    assert rc == 0
+    _cmp_run(got, want)
+    assert got["best_cost"] == best
+
+
+def test_evolve_blocks_paper_shape_matches_reference(ctx, pm, oracle, reflib):
+    """All 60 blocks of the paper's GA shape (nt=256: 8 crossover rounds, 8
+    mutation attempts) at 900/90, block for block against the reference's
+    evolve_block.  Guards the crossover kernel at scale: an earlier form of
+    it produced children with the wrong popcount in some processes."""
+    from paper_1610_10061_b200 import synth
+    costs = synth.euclid_costs(900, 12345)
+    ctx.set_instance(costs, 900, 900, 90)
+    ri = reflib.create(900, 900, 90, costs)
+    nb, nt = 60, 256
+    blocks = synth.random_population(900, 90, nb * nt, seed=9)
+    for kernel in (0, 3):
+        got, bc, bt = ctx.evolve_blocks(blocks, pm.ga_config(nb=nb, nt=nt, seed=1), kernel)
+        for b in range(nb):
+            rc, want, _, wcost, wthread = ri.evolve_block(blocks[b * nt:(b + 1) * nt], nt, nb, 1, kernel, b, -1, -1)
+            assert rc == 0
+            assert (got[b * nt:(b + 1) * nt] == want).all(), (kernel, b)
+            assert bc[b] == wcost and bt[b] == wthread, (kernel, b)
