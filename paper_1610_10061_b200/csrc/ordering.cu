@@ -243,10 +243,11 @@ constexpr int kWsWarps = kSortThreads / 32;
 // (the warp multi-split trick) -- far cheaper than MATCH.ANY over 32 distinct
 // values, which the profile showed serialising.
 template <int kBits>
-__device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid) {
+__device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid, int nbits = kBits) {
   unsigned peers = __ballot_sync(kFull, valid);
 #pragma unroll
   for (int b = 0; b < kBits; ++b) {
+    if (b >= nbits) break;  // warp-uniform
     const bool bit = (d >> b) & 1u;
     const unsigned bal = __ballot_sync(kFull, bit);
     peers &= bit ? bal : ~bal;
@@ -275,21 +276,23 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     const int64_t* crow = costs + (size_t)r * m;
-    for (int x = tid; x < m; x += kSortThreads) A[x] = ((KeyT)(uint64_t)crow[x] << sitebits) | (KeyT)x;
-    __syncthreads();
+    // keys of the warp's slice, with the first pass's digit histogram (shared
+    // atomics: one per key, instead of a ballot ranking pass)
+    for (int d = lane; d < 256; d += 32) mycnt[d] = 0;
+    __syncwarp();
+    for (int x = s0 + lane; x < s1; x += 32) {
+      const KeyT key = ((KeyT)(uint64_t)crow[x] << sitebits) | (KeyT)x;
+      A[x] = key;
+      atomicAdd(&mycnt[(unsigned)(key >> sitebits) & dmask], 1u);
+    }
     KeyT* src = A;
     KeyT* dst = B;
     for (int q = 0; q < npasses; ++q) {
       const int shift = sitebits + q * dbits;
-      for (int d = lane; d < 256; d += 32) mycnt[d] = 0;
-      __syncwarp();
-      for (int x0 = s0; x0 < s1; x0 += 32) {
-        const int x = x0 + lane;
-        const bool valid = x < s1;
-        const unsigned d = valid ? (unsigned)(src[x] >> shift) & dmask : 0u;
-        const unsigned peers = digit_peers<8>(d, valid);
-        if (valid && (peers & lt) == 0) mycnt[d] += __popc(peers);
+      if (q > 0) {
+        for (int d = lane; d < 256; d += 32) mycnt[d] = 0;
         __syncwarp();
+        for (int x = s0 + lane; x < s1; x += 32) atomicAdd(&mycnt[(unsigned)(src[x] >> shift) & dmask], 1u);
       }
       __syncthreads();
       if (tid < 256) {  // exclusive prefix over warps per digit; digit totals
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(kSortThreads, 1)
           const bool valid = x < s1;
           const KeyT key = valid ? src[x] : KeyT(0);
           const unsigned d = valid ? (unsigned)(key >> shift) & dmask : 0u;
-          const unsigned peers = digit_peers<8>(d, valid);
+          const unsigned peers = digit_peers<8>(d, valid, dbits);
           const unsigned rank = __popc(peers & lt);
           if (valid) dst[mycnt[d] + rank] = key;
           __syncwarp();
@@ -399,7 +402,9 @@ static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void
   const size_t per = (size_t)bp.m * (sizeof(KeyT) + (kPayload ? 4 : 0)) * 2;
   const size_t smem = sort_smem_header() + per;
   if constexpr (!kPayload) {  // packed keys: the warp-slice radix sort
-    const int dbits = 8;  // 8-bit digits, fully unrolled ballots (npasses = ceil(costbits / 8))
+    // npasses = ceil(costbits / 8) passes of balanced digits (<= 8 bits: one
+    // ballot per digit bit in the ranking), e.g. 2 x 7 bits for 14-bit costs
+    const int dbits = bp.npasses ? (bp.costbits + bp.npasses - 1) / bp.npasses : 8;
     const size_t hs = sort_smem_header();
     if (bp.smem_path) {
       auto kern = k_build_rows_ws<KeyT, OrdT, DistT, true>;
