@@ -141,27 +141,24 @@ inline void unrank_combination(size_t m, size_t p, UBig r, uint64_t* words) {
 }
 
 // Pascal table for the device unranking kernel: C(x, y) for y <= p, x < m as
-// L-limb little-endian numbers, entry (y * m + x) * L (consecutive x adjacent,
-// so a warp testing 32 consecutive candidates reads one contiguous run),
-// followed by C(m, p) itself.
+// L-limb little-endian numbers, limb-major: limb i of C(x, y) at
+// (y * L + i) * m + x (a warp testing 32 consecutive candidates reads one
+// contiguous run per limb), followed by C(m, p) itself (L limbs).
 inline std::vector<uint64_t> binomial_table(size_t m, size_t p, size_t L) {
   std::vector<uint64_t> t(((p + 1) * m + 1) * L, 0);
-  auto at = [&](size_t x, size_t y) { return &t[(y * m + x) * L]; };
-  for (size_t x = 0; x < m; ++x) at(x, 0)[0] = 1;
+  auto at = [&](size_t x, size_t y, size_t i) -> uint64_t& { return t[(y * L + i) * m + x]; };
+  for (size_t x = 0; x < m; ++x) at(x, 0, 0) = 1;
   for (size_t y = 1; y <= p; ++y) {
     for (size_t x = 1; x < m; ++x) {  // C(x, y) = C(x-1, y-1) + C(x-1, y); C(0, y) = 0
-      const uint64_t* a = at(x - 1, y - 1);
-      const uint64_t* b = at(x - 1, y);
-      uint64_t* z = at(x, y);
       unsigned __int128 carry = 0;
       for (size_t i = 0; i < L; ++i) {
-        const unsigned __int128 s = (unsigned __int128)a[i] + b[i] + carry;
-        z[i] = (uint64_t)s;
+        const unsigned __int128 s = (unsigned __int128)at(x - 1, y - 1, i) + at(x - 1, y, i) + carry;
+        at(x, y, i) = (uint64_t)s;
         carry = s >> 64;
       }
     }
   }
-  binomial(m, p).export_limbs(&t[(p + 1) * m * L], L);
+  binomial(m, p).export_limbs(&t[(p + 1) * L * m], L);
   return t;
 }
 

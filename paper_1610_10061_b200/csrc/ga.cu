@@ -204,7 +204,8 @@ __global__ void k_popcount_check(const uint64_t* __restrict__ pop, int count, in
 // the next taken candidate is the first j with C(a-j, k+1) < X, after which
 // X -= C(a-j, k+1), a -= j+1, k -= 1.  One warp per chromosome tests 32
 // consecutive candidates per probe (one contiguous table run), so a draw costs
-// ~p dependent probes instead of ~m.  Same subsets as the reference's walk,
+// ~p dependent probes instead of ~m.  The table is limb-major ([y][limb][x]),
+// so each limb load of a probe is one contiguous 256-byte run.  Same subsets as the reference's walk,
 // bit for bit (tests/test_gpu_ga.py).
 template <int kL>
 __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ranks,
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
   const int idx = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (idx >= count) return;  // warp-uniform
-  const uint64_t* bound = table + (size_t)(p + 1) * m * L;
+  const uint64_t* bound = table + (size_t)(p + 1) * L * m;
   uint64_t X[kL];  // X = C(m, p) - r (every lane holds the same value)
   {
     uint64_t borrow = 0;
@@ -239,9 +240,9 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
     uint64_t cv[kL];
     int cmp = -1;  // sign of C(x, k+1) - X; C(x, .) = 0 for x < 0
     if (x >= 0) {
-      const uint64_t* cp = table + ((size_t)(k + 1) * m + x) * L;
+      const uint64_t* cp = table + (size_t)(k + 1) * L * m + x;  // limb i at cp[i * m]
 #pragma unroll
-      for (int i = 0; i < kL; ++i) cv[i] = i < L ? __ldg(cp + i) : 0;
+      for (int i = 0; i < kL; ++i) cv[i] = i < L ? __ldg(cp + (size_t)i * m) : 0;
       cmp = 0;
 #pragma unroll
       for (int i = kL - 1; i >= 0; --i)
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
 // outputs are random-access -- output i is mix64(state0 + (i+1) * gamma) -- so
 // every attempt of a generation is tested at once and the accepted ones are
 // compacted in stream order; the stream position lives on the device
-// (rstate[0]), so no host work and no synchronisation are involved.
+// (rstate), so no host work and no synchronisation are involved.
 __device__ __forceinline__ void attempt_value(uint64_t state0, uint64_t first, int words, uint64_t top_mask,
                                               uint64_t* v /* little-endian, words limbs */) {
   for (int w = 0; w < words; ++w) {
@@ -298,68 +299,69 @@ __device__ __forceinline__ void attempt_value(uint64_t state0, uint64_t first, i
   }
 }
 
-__global__ void k_rank_flags(uint64_t state0, const unsigned long long* __restrict__ rstate, int words,
-                             uint64_t top_mask, const uint64_t* __restrict__ bound, int L, int A,
-                             uint32_t* __restrict__ flags) {
+// rstate: {stream position for even generations, for odd ones, shortfall
+// flag}; generation g reads slot g&1 and writes slot (g+1)&1, so the blocks of
+// one compaction never see a position updated under them.
+__global__ void __launch_bounds__(256) k_rank_flags(uint64_t state0, const unsigned long long* __restrict__ rstate,
+                                                    int slot, int words, uint64_t top_mask,
+                                                    const uint64_t* __restrict__ bound, int L, int A,
+                                                    uint32_t* __restrict__ flags, uint32_t* __restrict__ blockcnt) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= A) return;
-  uint64_t v[32];
-  attempt_value(state0, rstate[0] + (uint64_t)a * words, words, top_mask, v);
-  int cmp = 0;  // sign of v - bound, most significant limb first
-  for (int i = L - 1; i >= 0 && cmp == 0; --i) {
-    const uint64_t x = i < words ? v[i] : 0, b = bound[i];
-    cmp = x < b ? -1 : (x > b ? 1 : 0);
+  int cmp = 1;
+  if (a < A) {
+    uint64_t v[32];
+    attempt_value(state0, rstate[slot] + (uint64_t)a * words, words, top_mask, v);
+    cmp = 0;  // sign of v - bound, most significant limb first
+    for (int i = L - 1; i >= 0 && cmp == 0; --i) {
+      const uint64_t x = i < words ? v[i] : 0, b = bound[i];
+      cmp = x < b ? -1 : (x > b ? 1 : 0);
+    }
+    flags[a] = cmp < 0;
   }
-  flags[a] = cmp < 0;
+  const int c = __syncthreads_count(cmp < 0);
+  if (threadIdx.x == 0) blockcnt[blockIdx.x] = (uint32_t)c;
 }
 
-// One block: stream-order compaction of the accepted attempts; ranks [lo, hi)
-// of the population are written (islands keep their own slice), and the
-// stream position advances past the total-th accepted attempt.
-__global__ void __launch_bounds__(1024) k_rank_compact(uint64_t state0, unsigned long long* __restrict__ rstate,
-                                                       int words, uint64_t top_mask, int L, int A,
-                                                       const uint32_t* __restrict__ flags, int total, int lo,
-                                                       int hi, uint64_t* __restrict__ ranks) {
-  __shared__ uint32_t wsum[32];
-  __shared__ uint32_t grand;
+// Stream-order compaction of the accepted attempts, one thread per attempt:
+// ranks [lo, hi) of the population are written (islands keep their own
+// slice), and the next generation's stream position is the one just past the
+// total-th accepted attempt.
+__global__ void __launch_bounds__(256) k_rank_compact(uint64_t state0, unsigned long long* __restrict__ rstate,
+                                                      int slot, int words, uint64_t top_mask, int L, int A,
+                                                      const uint32_t* __restrict__ flags,
+                                                      const uint32_t* __restrict__ blockcnt, int total, int lo,
+                                                      int hi, uint64_t* __restrict__ ranks) {
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t pos = rstate[0];
-  const int seg = (A + blockDim.x - 1) / blockDim.x;
-  const int a0 = min(A, tid * seg), a1 = min(A, a0 + seg);
-  uint32_t cnt = 0;
-  for (int a = a0; a < a1; ++a) cnt += flags[a];
-  uint32_t incl = cnt;  // block exclusive scan of the per-thread counts
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += t;
+  if (warp == 0) {  // accepted attempts in the blocks before this one
+    uint32_t sacc = 0;
+    for (int b = lane; b < (int)blockIdx.x; b += 32) sacc += blockcnt[b];
+    sacc = warp_sum(sacc);
+    if (lane == 0) base = sacc;
   }
-  if (lane == 31) wsum[warp] = incl;
+  const int a = blockIdx.x * blockDim.x + tid;
+  const uint32_t f = a < A ? flags[a] : 0u;
+  const unsigned bal = __ballot_sync(kFull, f);
+  if (lane == 0) wsum[warp] = __popc(bal);
   __syncthreads();
-  if (warp == 0) {
-    uint32_t x = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0, xi = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, xi, o);
-      if (lane >= o) xi += t;
-    }
-    wsum[lane] = xi - x;
-    if (lane == 31) grand = xi;
-  }
-  __syncthreads();
-  uint32_t k = wsum[warp] + incl - cnt;
-  for (int a = a0; a < a1 && (int)k < total; ++a) {
-    if (!flags[a]) continue;
+  uint32_t k = base + __popc(bal & lanemask_lt());
+  for (int w = 0; w < warp; ++w) k += wsum[w];
+  const uint64_t pos = rstate[slot];
+  if (f && (int)k < total) {
     if ((int)k >= lo && (int)k < hi) {
       uint64_t v[32];
       attempt_value(state0, pos + (uint64_t)a * words, words, top_mask, v);
       uint64_t* dst = ranks + (size_t)(k - lo) * L;
       for (int i = 0; i < L; ++i) dst[i] = i < words ? v[i] : 0;
     }
-    if ((int)k == total - 1) rstate[0] = pos + (uint64_t)(a + 1) * words;
-    ++k;
+    if ((int)k == total - 1) rstate[slot ^ 1] = pos + (uint64_t)(a + 1) * words;
   }
-  if (tid == 0 && grand < (uint32_t)total) rstate[1] = 1;  // window exhausted (checked by the host)
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) {  // window exhausted (checked by the host)
+    uint32_t all = base;
+    for (int w = 0; w < 8; ++w) all += wsum[w];
+    if (all < (uint32_t)total) rstate[2] = 1;
+  }
 }
 
 static unsigned cdiv(size_t a, unsigned b) { return (unsigned)((a + b - 1) / b); }
@@ -382,7 +384,9 @@ static int lg2(size_t v) {
 // One evolve_block over every local block (kernel index `kernel`).
 static int evolve_all(pm_ctx* c, GaBuffers& B, const GaShape& s, uint64_t kernel) {
   const size_t count = (size_t)s.nbl * s.nt;
-  const unsigned tb = 256;
+  // one thread per chromosome; 64-thread blocks spread the 15,360 threads of
+  // the paper's shape over all SMs (256-thread blocks left 88 SMs idle)
+  const unsigned tb = 64;
   uint64_t* pop = B.pop.as<uint64_t>();
   int64_t* cost = B.cost.as<int64_t>();
   unsigned long long* evals = B.evals.as<unsigned long long>();
@@ -605,8 +609,8 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     PM_CUDA_TRY(c, B.table.ensure(tab.size() * 8));
     PM_CUDA_TRY(c, B.ranks.ensure(count * hd.L * 8));
     PM_CUDA_TRY(c, cudaMemcpy(B.table.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
-    PM_CUDA_TRY(c, B.rstate.ensure(16));  // {stream position, window-exhausted flag}
-    PM_CUDA_TRY(c, cudaMemsetAsync(B.rstate.p, 0, 16, c->stream));
+    PM_CUDA_TRY(c, B.rstate.ensure(24));  // {position (even gen), position (odd gen), shortfall}
+    PM_CUDA_TRY(c, cudaMemsetAsync(B.rstate.p, 0, 24, c->stream));
   }
   auto draw = [&](DevBuf& dst, uint64_t generation) -> int {
     if (ref_draw && hd.L) {
@@ -614,15 +618,17 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
       // attempts window: the accepted count falls short of `total` with
       // probability < 1e-30 (12 sigma); a shortfall is reported, never ignored
       const int A = (int)std::ceil((total + 12.0 * std::sqrt((double)total) + 64.0) / hd.accept);
-      PM_CUDA_TRY(c, B.rflags.ensure((size_t)A * 4));
+      const unsigned G = cdiv(A, 256);
+      PM_CUDA_TRY(c, B.rflags.ensure(((size_t)A + G) * 4));
+      uint32_t* flags = B.rflags.as<uint32_t>();
+      uint32_t* blockcnt = flags + A;
+      const int slot = (int)(generation & 1);
       const uint64_t* bound = B.table.as<uint64_t>() + (size_t)(s.p + 1) * s.m * L;
-      k_rank_flags<<<cdiv(A, 256), 256, 0, c->stream>>>(hd.stream.state, B.rstate.as<unsigned long long>(),
-                                                       hd.words, hd.top_mask, bound, L, A,
-                                                       B.rflags.as<uint32_t>());
-      k_rank_compact<<<1, 1024, 0, c->stream>>>(hd.stream.state, B.rstate.as<unsigned long long>(), hd.words,
-                                                hd.top_mask, L, A, B.rflags.as<uint32_t>(), total,
-                                                (int)(block0 * nt), (int)((block0 + nbl) * nt),
-                                                B.ranks.as<uint64_t>());
+      k_rank_flags<<<G, 256, 0, c->stream>>>(hd.stream.state, B.rstate.as<unsigned long long>(), slot, hd.words,
+                                             hd.top_mask, bound, L, A, flags, blockcnt);
+      k_rank_compact<<<G, 256, 0, c->stream>>>(hd.stream.state, B.rstate.as<unsigned long long>(), slot, hd.words,
+                                               hd.top_mask, L, A, flags, blockcnt, total, (int)(block0 * nt),
+                                               (int)((block0 + nbl) * nt), B.ranks.as<uint64_t>());
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 2;
       const unsigned g = cdiv(count * 32, 256);
@@ -635,7 +641,7 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
       hd.draw(nb * nt, block0 * nt, (block0 + nbl) * nt, host_pop.data());
       PM_CUDA_TRY(c, cudaMemcpyAsync(dst.p, host_pop.data(), count * wp * 8, cudaMemcpyHostToDevice, c->stream));
     } else {
-      k_draw_population<<<cdiv(count, 256), 256, 0, c->stream>>>(dst.as<uint64_t>(), (int)count, (int)wp, s.m,
+      k_draw_population<<<cdiv(count, 64), 64, 0, c->stream>>>(dst.as<uint64_t>(), (int)count, (int)wp, s.m,
                                                                   s.p, cfg->seed, generation, block0 * nt);
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 1;
@@ -711,12 +717,12 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     }
     std::swap(B.pop, B.next);
   }
-  unsigned long long ref_evals = 0, rstate[2] = {0, 0};
+  unsigned long long ref_evals = 0, rstate[3] = {0, 0, 0};
   PM_CUDA_TRY(c, cudaMemcpyAsync(&ref_evals, B.evals.p, 8, cudaMemcpyDeviceToHost, c->stream));
   if (ref_draw && hd.L)
-    PM_CUDA_TRY(c, cudaMemcpyAsync(rstate, B.rstate.p, 16, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA_TRY(c, cudaMemcpyAsync(rstate, B.rstate.p, 24, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (rstate[1]) return c->fail(PM_CUDA, "population draw: attempt window exhausted");
+  if (rstate[2]) return c->fail(PM_CUDA, "population draw: attempt window exhausted");
   size_t fb = 0;
   rc = pm_check_errors(c, &fb);
   if (rc) return rc;
