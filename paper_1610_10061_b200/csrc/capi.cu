@@ -54,9 +54,11 @@ void pm_destroy(pm_ctx* c) {
   for (DevBuf* b : {&c->ord, &c->dist, &c->dT, &c->costs_in, &c->sort_keys, &c->sort_pay, &c->words,
                     &c->costs_out, &c->T, &c->lists, &c->counts, &c->errw, &c->scal, &c->ga.pop,
                     &c->ga.next, &c->ga.cost, &c->ga.before, &c->ga.child, &c->ga.ccost, &c->ga.ok,
-                    &c->ga.bcost, &c->ga.bthread, &c->ga.bwords, &c->ga.evals, &c->ga.tmp,
-                    &c->ga.table, &c->ga.ranks})
+                    &c->ga.brec, &c->ga.evals, &c->ga.tmp, &c->ga.table, &c->ga.ranks, &c->ga.rflags,
+                    &c->ga.rstate})
     b->release();
+  c->ga.hrec.release();
+  c->ga.hmig.release();
   for (auto* v : {&c->ev_used, &c->ev_free})
     for (auto& e : *v) {
       cudaEventDestroy(e.first);

@@ -49,9 +49,36 @@ using pmb::DevTables;
 using pmb::BuildPlan;
 
 namespace pmb {
-// GA working set (ga.cu), grow-only and kept across calls.
+// Pinned host staging (grow-only): one transfer per generation for the
+// block-best records and for migration.
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocDefault);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// GA working set (ga.cu), grow-only and kept across calls.  brec holds one
+// record {cost, thread, words[wp]} per block (k_block_min).
 struct GaBuffers {
-  DevBuf pop, next, cost, before, child, ccost, ok, bcost, bthread, bwords, evals, tmp, table, ranks, rflags, rstate;
+  DevBuf pop, next, cost, before, child, ccost, ok, brec, evals, tmp, table, ranks, rflags, rstate;
+  HostBuf hrec, hmig;
 };
 }  // namespace pmb
 using pmb::GaBuffers;

@@ -111,9 +111,10 @@ __global__ void k_mutation_accept(uint64_t* __restrict__ pop, int64_t* __restric
 }
 
 // block_min_reduce (ga.cpp:113-134): lexicographic (cost, thread) minimum.
+// Writes block b's record {cost, thread, words[wp]} at rec + b * (2 + wp): the
+// layout the islands exchange, copied to the host in one transfer.
 __global__ void k_block_min(const int64_t* __restrict__ cost, const uint64_t* __restrict__ pop, int nt,
-                            int wp, int64_t* __restrict__ bcost, uint64_t* __restrict__ bthread,
-                            uint64_t* __restrict__ bwords) {
+                            int wp, uint64_t* __restrict__ rec) {
   __shared__ int64_t sc[32];
   __shared__ int st[32];
   const int b = blockIdx.x;
@@ -155,13 +156,14 @@ __global__ void k_block_min(const int64_t* __restrict__ cost, const uint64_t* __
     if (lane == 0) {
       sc[0] = best;
       st[0] = bt;
-      bcost[b] = best;
-      bthread[b] = (uint64_t)bt;
+      rec[(size_t)b * (2 + wp)] = (uint64_t)best;
+      rec[(size_t)b * (2 + wp) + 1] = (uint64_t)bt;
     }
   }
   __syncthreads();
   const int t = st[0];
-  for (int w = threadIdx.x; w < wp; w += blockDim.x) bwords[(size_t)b * wp + w] = pop[((size_t)b * nt + t) * wp + w];
+  for (int w = threadIdx.x; w < wp; w += blockDim.x)
+    rec[(size_t)b * (2 + wp) + 2 + w] = pop[((size_t)b * nt + t) * wp + w];
 }
 
 // Device-native population draw: uniform p-subsets by Floyd's algorithm from a
@@ -421,8 +423,7 @@ static int evolve_all(pm_ctx* c, GaBuffers& B, const GaShape& s, uint64_t kernel
     PM_CUDA_TRY(c, cudaGetLastError());
     c->launches += 2;
   }
-  k_block_min<<<s.nbl, 256, 0, c->stream>>>(cost, pop, s.nt, s.wp, B.bcost.as<int64_t>(),
-                                              B.bthread.as<uint64_t>(), B.bwords.as<uint64_t>());
+  k_block_min<<<s.nbl, 256, 0, c->stream>>>(cost, pop, s.nt, s.wp, B.brec.as<uint64_t>());
   PM_CUDA_TRY(c, cudaGetLastError());
   c->launches += 1;
   return PM_OK;
@@ -438,9 +439,7 @@ static int ga_alloc(pm_ctx* c, GaBuffers& B, const GaShape& s) {
   PM_CUDA_TRY(c, B.child.ensure(kids * s.wp * 8));
   PM_CUDA_TRY(c, B.ccost.ensure(kids * 8));
   PM_CUDA_TRY(c, B.ok.ensure(count));
-  PM_CUDA_TRY(c, B.bcost.ensure((size_t)s.nbl * 8));
-  PM_CUDA_TRY(c, B.bthread.ensure((size_t)s.nbl * 8));
-  PM_CUDA_TRY(c, B.bwords.ensure((size_t)s.nbl * s.wp * 8));
+  PM_CUDA_TRY(c, B.brec.ensure((size_t)s.nbl * (2 + s.wp) * 8));
   PM_CUDA_TRY(c, B.evals.ensure(16));
   PM_CUDA_TRY(c, B.tmp.ensure(16));
   return PM_OK;
@@ -564,18 +563,17 @@ int pm_evolve_blocks(pm_ctx* c, uint64_t* blocks, size_t nb, size_t words_per, c
   if (rc) {
     return rc;
   }
-  std::vector<int64_t> bc(nb);
-  std::vector<uint64_t> bt(nb);
+  const size_t rec = 2 + (size_t)s.wp;
+  std::vector<uint64_t> hr(nb * rec);
   PM_CUDA_TRY(c, cudaMemcpyAsync(blocks, B.pop.p, count * s.wp * 8, cudaMemcpyDeviceToHost, c->stream));
-  PM_CUDA_TRY(c, cudaMemcpyAsync(bc.data(), B.bcost.p, nb * 8, cudaMemcpyDeviceToHost, c->stream));
-  PM_CUDA_TRY(c, cudaMemcpyAsync(bt.data(), B.bthread.p, nb * 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(hr.data(), B.brec.p, nb * rec * 8, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   size_t fb = 0;
   rc = pm_check_errors(c, &fb);
   if (rc) return rc;
   for (size_t b = 0; b < nb; ++b) {
-    if (best_cost) best_cost[b] = bc[b];
-    if (best_thread) best_thread[b] = (size_t)bt[b];
+    if (best_cost) best_cost[b] = (int64_t)hr[b * rec];
+    if (best_thread) best_thread[b] = (size_t)hr[b * rec + 1];
   }
   return PM_OK;
 }
@@ -653,11 +651,14 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
   rc = draw(B.pop, 0);
   if (rc) return rc;
 
-  // per-block record exchanged between islands: {cost, thread, words[wp]}
+  // per-block record exchanged between islands: {cost, thread, words[wp]},
+  // written by k_block_min and copied to pinned memory in one transfer
   const size_t rec = 2 + wp;
-  std::vector<uint64_t> local(nbl * rec), global(nb * rec);
-  std::vector<int64_t> bc(nbl);
-  std::vector<uint64_t> bt(nbl), bw(nbl * wp);
+  PM_CUDA_TRY(c, B.hrec.ensure(nbl * rec * 8));
+  PM_CUDA_TRY(c, B.hmig.ensure(nb * wp * 8));
+  const uint64_t* local = B.hrec.as<uint64_t>();
+  uint64_t* mig = B.hmig.as<uint64_t>();
+  std::vector<uint64_t> global(nb * rec);
   int64_t best_cost = std::numeric_limits<int64_t>::max();
   std::vector<uint64_t> best(wp, 0);
   size_t stale = 0, kernels = 0, kernel_of_best = 0;
@@ -672,21 +673,14 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     // draw the next population while the device evolves (ga.cpp:274)
     rc = draw(B.next, kernel + 1);
     if (rc) return rc;
-    PM_CUDA_TRY(c, cudaMemcpyAsync(bc.data(), B.bcost.p, nbl * 8, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA_TRY(c, cudaMemcpyAsync(bt.data(), B.bthread.p, nbl * 8, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA_TRY(c, cudaMemcpyAsync(bw.data(), B.bwords.p, nbl * wp * 8, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA_TRY(c, cudaMemcpyAsync(B.hrec.p, B.brec.p, nbl * rec * 8, cudaMemcpyDeviceToHost, c->stream));
     PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     evolve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - g0).count();
-    for (size_t b = 0; b < nbl; ++b) {
-      local[b * rec] = (uint64_t)bc[b];
-      local[b * rec + 1] = bt[b];
-      std::memcpy(&local[b * rec + 2], &bw[b * wp], wp * 8);
-    }
     if (world > 1) {
-      if (allgather(local.data(), local.size() * 8, global.data(), user) != 0)
+      if (allgather(B.hrec.p, nbl * rec * 8, global.data(), user) != 0)
         return c->fail(PM_NCCL, "island allgather failed");
     } else {
-      global = local;
+      std::memcpy(global.data(), local, nbl * rec * 8);
     }
     size_t best_block = 0;  // ga.cpp:279-282: strict <, lowest block wins ties
     for (size_t b = 1; b < nb; ++b)
@@ -705,15 +699,16 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
       kernels = (size_t)kernel + 1;
       break;
     }
-    // migrate (ga.cpp:204-215) into the freshly drawn population
+    // migrate (ga.cpp:204-215) into the freshly drawn population: one
+    // transfer from pinned staging (block b's best to slot 0 of block b, or
+    // in team mode every block's best to slots 0..nb-1 of block 0)
     if (cfg->migration == PM_MIGRATE_BLOCK) {
-      for (size_t b = 0; b < nbl; ++b)
-        PM_CUDA_TRY(c, cudaMemcpyAsync(B.next.as<uint64_t>() + (b * nt) * wp, &global[(block0 + b) * rec + 2],
-                                       wp * 8, cudaMemcpyHostToDevice, c->stream));
+      for (size_t b = 0; b < nbl; ++b) std::memcpy(&mig[b * wp], &global[(block0 + b) * rec + 2], wp * 8);
+      PM_CUDA_TRY(c, cudaMemcpy2DAsync(B.next.p, nt * wp * 8, mig, wp * 8, wp * 8, nbl, cudaMemcpyHostToDevice,
+                                       c->stream));
     } else if (rank == 0) {
-      for (size_t b = 0; b < nb; ++b)
-        PM_CUDA_TRY(c, cudaMemcpyAsync(B.next.as<uint64_t>() + b * wp, &global[b * rec + 2], wp * 8,
-                                       cudaMemcpyHostToDevice, c->stream));
+      for (size_t b = 0; b < nb; ++b) std::memcpy(&mig[b * wp], &global[b * rec + 2], wp * 8);
+      PM_CUDA_TRY(c, cudaMemcpyAsync(B.next.p, mig, nb * wp * 8, cudaMemcpyHostToDevice, c->stream));
     }
     std::swap(B.pop, B.next);
   }
