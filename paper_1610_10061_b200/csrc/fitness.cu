@@ -30,6 +30,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <utility>
 #include <vector>
 
@@ -385,31 +386,45 @@ static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool t
 
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode) {
   ScanPlan sp;
-  // (group width, warps, masks in smem?) in preference order.  Measured on
-  // B200 (profiles/): 32-wide groups beat 64-wide at every BASELINE shape
-  // (64-wide doubles the mask and counter footprint and the per-lane hit
-  // bursts), and a CTA must leave L1 room for the lanes' in-flight row
-  // prefetches -- shared memory above ~200 KB halves throughput.  The last
-  // entry reads the masks from global memory and always fits.
-  const struct { int G, warps; bool tsmem; } shapes[] = {
-      {32, 16, true}, {32, 14, true}, {32, 12, true}, {32, 10, true}, {32, 8, true},
-      {32, 6, true},  {32, 4, true},  {32, 8, false}};
+  // (group width, warps per CTA, CTAs per SM, masks in smem?) in preference
+  // order.  Measured on B200 (profiles/r01_ncu_kernels.md):
+  // * 32-wide groups beat 64-wide at every BASELINE shape (64-wide doubles the
+  //   mask and counter footprint and the per-lane hit bursts);
+  // * a CTA must leave L1 room for the lanes' in-flight row prefetches --
+  //   shared memory above ~200 KB halves throughput;
+  // * when a CTA segment (its share of one group's clients) is short -- small
+  //   n (pmed40) or few units per CTA (syn5k) -- the per-segment barriers leave
+  //   warps idle, so the same 16 warps per SM run as 8 x 2 or 4 x 4 CTAs whose
+  //   barriers overlap (pmed40 0.114 -> 0.082 ms, syn5k 0.181 -> 0.161 ms);
+  //   with long segments (>= 4096 clients) splitting is neutral, so one CTA
+  //   per SM is kept there.
+  // The last entry reads the masks from global memory and always fits.
+  const struct { int G, warps, cps; bool tsmem; } shapes[] = {
+      {32, 2, 8, true}, {32, 4, 4, true}, {32, 8, 2, true},
+      {32, 16, 1, true}, {32, 14, 1, true}, {32, 12, 1, true}, {32, 10, 1, true}, {32, 8, 1, true},
+      {32, 6, 1, true},  {32, 4, 1, true},  {32, 8, 1, false}};
   const size_t chunk_bytes = (size_t)kChunk * (t.site_bytes + t.dist_bytes);
   const size_t l1_total = 228 * 1024;
-  const int ctas = sms;
   const unsigned long long vmax = depth_mode ? (unsigned long long)t.Wp : (unsigned long long)t.max_cost;
-  // PMB_SCAN_SHAPE="G,warps" pins the shape (tuning experiments only)
+  // clients per CTA segment (a segment never crosses a group)
+  const long long units_per_sm = ((long long)((count + 31) / 32) * t.n + sms - 1) / sms;
+  const bool split = std::min<long long>(units_per_sm, t.n) < 4096;
+  // PMB_SCAN_SHAPE="G,warps[,ctas per SM]" pins the shape (tuning experiments only)
   const char* force = getenv("PMB_SCAN_SHAPE");
-  int fG = 0, fW = 0;
-  if (force) sscanf(force, "%d,%d", &fG, &fW);
+  int fG = 0, fW = 0, fC = 1;
+  if (force) sscanf(force, "%d,%d,%d", &fG, &fW, &fC);
   for (const auto& sh0 : shapes) {
     auto sh = sh0;
     if (fG) {
       if (&sh0 != &shapes[0]) break;
       sh.G = fG;
       sh.warps = fW;
+      sh.cps = std::max(1, fC);
       sh.tsmem = true;
+    } else if (sh.cps > 1 && !split) {
+      continue;
     }
+    const int ctas = sms * sh.cps;
     const size_t groups = (count + sh.G - 1) / sh.G;
     const long long U = (long long)groups * t.n;
     const long long seg = (U + ctas - 1) / ctas;  // clients one lane counter can see (upper bound)
@@ -418,8 +433,11 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
           pass == 0 && (unsigned long long)std::min<long long>(seg, t.n) * vmax < (1ull << 32);
       if (pass == 0 && !acc32) continue;
       const size_t smem = scan_smem(t.m, sh.warps, acc32, sh.tsmem, sh.G);
-      const size_t inflight = (size_t)sh.warps * 32 * chunk_bytes / 2;  // L1 room for in-flight row loads
-      if (smem <= max_smem && (fG || !sh.tsmem || smem + inflight <= l1_total)) {
+      // shared memory of all CTAs on the SM (+1 KB reserved each) plus L1 room
+      // for the in-flight row loads of all their warps
+      const size_t inflight = (size_t)sh.cps * sh.warps * 32 * chunk_bytes / 2;
+      const size_t resident = (size_t)sh.cps * (smem + 1024);
+      if (smem <= max_smem && (fG || !sh.tsmem || resident + inflight <= l1_total)) {
         sp.G = sh.G;
         sp.tsmem = sh.tsmem;
         sp.warps = sh.warps;
