@@ -347,7 +347,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-GA_GENS = 5
+GA_GENS = 20
 
 
 def bench_ga(ctx, args, world, rank, local, n, m, p):

@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstddef>
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -143,7 +144,8 @@ inline void unrank_combination(size_t m, size_t p, UBig r, uint64_t* words) {
 // Pascal table for the device unranking kernel: C(x, y) for y <= p, x < m as
 // L-limb little-endian numbers, limb-major: limb i of C(x, y) at
 // (y * L + i) * m + x (a warp testing 32 consecutive candidates reads one
-// contiguous run per limb), followed by C(m, p) itself (L limbs).
+// contiguous run per limb), followed by C(m, p) itself (L limbs) and the
+// per-step limb counts.
 inline std::vector<uint64_t> binomial_table(size_t m, size_t p, size_t L) {
   std::vector<uint64_t> t(((p + 1) * m + 1) * L, 0);
   auto at = [&](size_t x, size_t y, size_t i) -> uint64_t& { return t[(y * L + i) * m + x]; };
@@ -159,6 +161,14 @@ inline std::vector<uint64_t> binomial_table(size_t m, size_t p, size_t L) {
     }
   }
   binomial(m, p).export_limbs(&t[(p + 1) * L * m], L);
+  // then, per k < p, the limbs of C(m, k + 1): every value of step k of the
+  // unranking (X and the probed C(x, k + 1)) fits in that many limbs
+  UBig c(1);
+  for (size_t k = 0; k < p; ++k) {  // C(m, k + 1) = C(m, k) * (m - k) / (k + 1)
+    c.mul(m - k);
+    c.div(k + 1);
+    t.push_back(std::max<size_t>(1, c.limbs()));
+  }
   return t;
 }
 

@@ -209,6 +209,76 @@ __global__ void k_popcount_check(const uint64_t* __restrict__ pop, int count, in
 // ~p dependent probes instead of ~m.  The table is limb-major ([y][limb][x]),
 // so each limb load of a probe is one contiguous 256-byte run.  Same subsets as the reference's walk,
 // bit for bit (tests/test_gpu_ga.py).
+// One probe of 32 consecutive candidates with kN-limb arithmetic (X and the
+// probed binomials fit in kN limbs at this step); on a hit, X -= C(a-j, k+1)
+// and the lane index of the taken candidate is returned, else -1.
+template <int kN, int kL>
+__device__ __forceinline__ int unrank_probe(const uint64_t* __restrict__ table, int m, int L, int k, int x,
+                                            uint64_t (&X)[kL]) {
+  uint64_t cv[kN];
+  int cmp = -1;  // sign of C(x, k+1) - X; C(x, .) = 0 for x < 0
+  if (x >= 0) {
+    const uint64_t* cp = table + (size_t)(k + 1) * L * m + x;  // limb i at cp[i * m]
+#pragma unroll
+    for (int i = 0; i < kN; ++i) cv[i] = i < L ? __ldg(cp + (size_t)i * m) : 0;  // bucket may exceed L
+    cmp = 0;
+#pragma unroll
+    for (int i = kN - 1; i >= 0; --i)
+      if (cmp == 0) cmp = cv[i] < X[i] ? -1 : (cv[i] > X[i] ? 1 : 0);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kN; ++i) cv[i] = 0;
+  }
+  const unsigned hit = __ballot_sync(kFull, cmp < 0);
+  if (!hit) return -1;
+  const int jl = __ffs(hit) - 1;
+  uint64_t borrow = 0;
+#pragma unroll
+  for (int i = 0; i < kN; ++i) {
+    const uint64_t v = __shfl_sync(kFull, cv[i], jl);
+    const uint64_t d = X[i] - v - borrow;
+    borrow = (X[i] < v) || (X[i] - v < borrow);
+    X[i] = d;
+  }
+  return jl;
+}
+
+// Dispatch on the step's limb count (warp-uniform): the smallest instantiated
+// width that holds it.
+template <int kL>
+__device__ __forceinline__ int unrank_probe_n(int lim, const uint64_t* __restrict__ table, int m, int L, int k,
+                                              int x, uint64_t (&X)[kL]) {
+  if (lim <= 1) return unrank_probe<1, kL>(table, m, L, k, x, X);
+  if (lim <= 2) return unrank_probe<2, kL>(table, m, L, k, x, X);
+  if constexpr (kL >= 4) {
+    if (lim <= 3) return unrank_probe<3, kL>(table, m, L, k, x, X);
+    if (lim <= 4) return unrank_probe<4, kL>(table, m, L, k, x, X);
+  }
+  if constexpr (kL >= 8) {
+    if (lim <= 6) return unrank_probe<6, kL>(table, m, L, k, x, X);
+    if (lim <= 8) return unrank_probe<8, kL>(table, m, L, k, x, X);
+  }
+  if constexpr (kL >= 16) {
+    if (lim <= 12) return unrank_probe<12, kL>(table, m, L, k, x, X);
+    if (lim <= 16) return unrank_probe<16, kL>(table, m, L, k, x, X);
+  }
+  if constexpr (kL >= 32) {
+    if (lim <= 24) return unrank_probe<24, kL>(table, m, L, k, x, X);
+  }
+  return unrank_probe<kL, kL>(table, m, L, k, x, X);
+}
+
+// Reference-exact unranking on the device (combinatorics.cpp:20-52): the
+// rank-th p-subset of {0..m-1} in lexicographic order.  The reference walks
+// the candidates one by one (take candidate when C(a, k) > r, else
+// r -= C(a, k)); a run of skips telescopes (hockey stick:
+// sum_{t<j} C(a-t, k) = C(a+1, k+1) - C(a-j+1, k+1)), so with X = C(a+1, k+1) - r
+// the next taken candidate is the first j with C(a-j, k+1) < X, after which
+// X -= C(a-j, k+1), a -= j+1, k -= 1.  One warp per chromosome tests 32
+// consecutive candidates per probe (one contiguous table run per limb), so a
+// draw costs ~p dependent probes instead of ~m, each with only the limbs the
+// step's values need (X < C(m, k+1) shrinks as k falls).  Same subsets as the
+// reference's walk, bit for bit (tests/test_gpu_ga.py).
 template <int kL>
 __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ranks,
                                                 const uint64_t* __restrict__ table, int m, int p, int L, int wp,
@@ -217,6 +287,7 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
   const int lane = threadIdx.x & 31;
   if (idx >= count) return;  // warp-uniform
   const uint64_t* bound = table + (size_t)(p + 1) * L * m;
+  const uint64_t* lims = bound + L;  // limbs of C(m, k + 1), k < p
   uint64_t X[kL];  // X = C(m, p) - r (every lane holds the same value)
   {
     uint64_t borrow = 0;
@@ -237,38 +308,14 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
   int a = m - 1, k = p - 1, base = 0;
   int word_idx = 0;
   uint64_t word = 0;  // the output word being filled (candidates increase)
+  int lim = (int)__ldg(lims + k);
   while (k >= 0) {
-    const int x = a - base - lane;
-    uint64_t cv[kL];
-    int cmp = -1;  // sign of C(x, k+1) - X; C(x, .) = 0 for x < 0
-    if (x >= 0) {
-      const uint64_t* cp = table + (size_t)(k + 1) * L * m + x;  // limb i at cp[i * m]
-#pragma unroll
-      for (int i = 0; i < kL; ++i) cv[i] = i < L ? __ldg(cp + (size_t)i * m) : 0;
-      cmp = 0;
-#pragma unroll
-      for (int i = kL - 1; i >= 0; --i)
-        if (cmp == 0 && i < L) cmp = cv[i] < X[i] ? -1 : (cv[i] > X[i] ? 1 : 0);
-    } else {
-#pragma unroll
-      for (int i = 0; i < kL; ++i) cv[i] = 0;
-    }
-    const unsigned hit = __ballot_sync(kFull, cmp < 0);
-    if (!hit) {
+    const int jl = unrank_probe_n<kL>(lim, table, m, L, k, a - base - lane, X);
+    if (jl < 0) {
       base += 32;
       continue;
     }
-    const int jl = __ffs(hit) - 1, j = base + jl;
-    uint64_t borrow = 0;  // X -= C(a - j, k + 1), the limbs from lane jl
-#pragma unroll
-    for (int i = 0; i < kL; ++i) {
-      if (i < L) {
-        const uint64_t v = __shfl_sync(kFull, cv[i], jl);
-        const uint64_t d = X[i] - v - borrow;
-        borrow = (X[i] < v) || (X[i] - v < borrow);
-        X[i] = d;
-      }
-    }
+    const int j = base + jl;
     const int cand = m - 1 - a + j;
     if ((cand >> 6) != word_idx) {
       if (lane == 0 && word) w[word_idx] = word;
@@ -279,6 +326,7 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
     a -= j + 1;
     --k;
     base = 0;
+    if (k >= 0) lim = (int)__ldg(lims + k);
   }
   if (lane == 0 && word) w[word_idx] = word;
 }
