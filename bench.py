@@ -303,6 +303,9 @@ def run_ours(args):
         del so, inc
 
     ga = None if args.no_ga else bench_ga(ctx, args, world, rank, local, n, m, p)
+    evolved = None
+    if rank == 0 and world == 1 and not args.no_ga and count % 256 == 0:
+        evolved = evolved_population(ctx, pop, n, wp, stream, flush, args.steps, peak)
 
     clocks = clk.summary()
     line = {
@@ -338,6 +341,7 @@ def run_ours(args):
         "clocks": clocks,
         "clocks_e2e": clk2.summary(),
         "ga": ga,
+        "evolved_population": evolved,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -406,6 +410,47 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
             "optimum_by": f"device evaluation of all {nsub} p-subsets ({t_ex:.1f} s incl. host enumeration)"}
         c3.close()
     return out
+
+
+def evolved_population(ctx, pop, n, wp, stream, flush, steps, peak):
+    """SURVEY.md 8(d) secondary report: the same batch after 3 reference
+    evolve_block generations (nt=256); evolved chromosomes keep clients near
+    an open site, so k* is shorter than for uniform random subsets."""
+    import torch
+
+    import paper_1610_10061_b200 as pm
+    count = pop.shape[0]
+    cfg = pm.ga_config(nb=count // 256, nt=256, seed=1)
+    ev = pop
+    for kern in range(3):
+        ev, _, _ = ctx.evolve_blocks(ev, cfg, kern)
+    w = torch.from_numpy(np.ascontiguousarray(ev).view(np.int64)).cuda()
+    out = torch.empty(count, dtype=torch.int64, device="cuda")
+    sumk = torch.empty(count, dtype=torch.int64, device="cuda")
+    ctx.scan_depths_device(w, sumk, count, wp)
+    ks = int(sumk.sum().item())
+    for _ in range(3):
+        ctx.evaluate_device(w, out, count, wp, check=False)
+    ctx.profile_read()
+    ctx.set_profiling(True)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for s in range(steps):
+        flush.zero_()
+        ev0[s].record(stream)
+        ctx.evaluate_device(w, out, count, wp, check=False)
+        ev1[s].record(stream)
+    torch.cuda.synchronize()
+    ctx.set_profiling(False)
+    kern_ms, kern_n = ctx.profile_read()
+    ctx.check_errors()
+    ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1)) / steps
+    kern_s = kern_ms / max(1, kern_n) / 1e3
+    achieved = (12 * ks + 8 * wp * count) / kern_s / 1e9
+    return {"config": f"the benchmark batch after 3 evolve_block generations (nb={count // 256}, nt=256, seed 1)",
+            "evals_per_s": count / (ms / 1e3), "mean_k_star": ks / (count * n),
+            "roofline_frac": achieved / peak}
 
 
 def exhaustive_optimum(ctx, m, p):
