@@ -365,7 +365,16 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
     nb = 16 * world
     cfg = pm.ga_config(nb=nb, nt=256, evolve_limit=GA_GENS, saturation=GA_GENS + 1, seed=1,
                        population="device")
-    ag = None if world == 1 else pm.torch_allgather(device=f"cuda:{local}" if BACKEND == "nccl" else None)
+    ag = None
+    if world > 1 and BACKEND == "nccl":
+        # the library's own NCCL exchange (pm_nccl_*); torch.distributed only
+        # distributes the communicator's unique id
+        import torch.distributed as dist
+        box = [pm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        ag = pm.NcclComm(box[0], rank, world, local)
+    elif world > 1:
+        ag = pm.torch_allgather()  # gloo (CPU test runs)
     warm = pm.ga_config(nb=nb, nt=256, evolve_limit=1, saturation=1, seed=2, population="device")
     ctx.run_ga(warm, rank=rank, world=world, allgather=ag)  # first launches load the GA kernels
     r = ctx.run_ga(cfg, rank=rank, world=world, allgather=ag)
@@ -373,7 +382,12 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
                       "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
                       "best_cost": r["best_cost"], "evals_per_gen_reference_semantics":
                           r["evaluations"] / r["kernels_executed"],
-                      "device_evals_per_gen": r["device_evaluations"] / r["kernels_executed"]}
+                      "device_evals_per_gen": r["device_evaluations"] / r["kernels_executed"],
+                      "exchange": "none (1 island)" if world == 1 else (
+                          "pm_nccl_allgather (library NCCL communicator)" if BACKEND == "nccl"
+                          else "torch.distributed gloo allgather")}
+    if isinstance(ag, pm.NcclComm):
+        ag.close()
     if world == 1 and rank == 0:
         # the paper's Table-1 shape (nb=60, nt=256) on a pmed40-sized synthetic instance
         import paper_1610_10061_b200 as pm2

@@ -208,6 +208,19 @@ typedef int (*pm_allgather_fn)(const void* send, size_t bytes, void* recv, void*
 int pm_run_ga_islands(pm_ctx* ctx, const pm_ga_config* cfg, int rank, int world, pm_allgather_fn allgather,
                       void* user, uint64_t* best_words, int64_t* per_kernel_best, pm_run_result* result);
 
+/* Native island exchange over NCCL (NVLink/NVSwitch on one node) for C/C++
+ * hosts without torch.distributed: one communicator per rank, created from a
+ * unique id that rank 0 generates and the launcher distributes (file, MPI,
+ * socket ...).  pm_nccl_allgather has the pm_allgather_fn shape; pass the
+ * pm_nccl* as `user`.  The record travels through device memory and one
+ * ncclAllGather on the communicator's stream.  PM_NCCL on failure. */
+#define PM_NCCL_ID_BYTES 128
+typedef struct pm_nccl pm_nccl;
+int pm_nccl_unique_id(char id[PM_NCCL_ID_BYTES]);
+int pm_nccl_create(const char id[PM_NCCL_ID_BYTES], int rank, int world, int device, pm_nccl** out);
+void pm_nccl_destroy(pm_nccl* comm);
+int pm_nccl_allgather(const void* send, size_t bytes, void* recv, void* user);
+
 #ifdef __cplusplus
 }
 #endif

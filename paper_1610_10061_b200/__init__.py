@@ -92,7 +92,8 @@ C_ABI_SYMBOLS = (
     "pm_evaluate", "pm_evaluate_device", "pm_check_errors", "pm_set_eval_kernel",
     "pm_auto_eval_kernel", "pm_min_cost_sum", "pm_scan_depths_device", "pm_set_profiling",
     "pm_profile_read", "pm_evolve_blocks", "pm_run_ga", "pm_run_ga_islands", "pm_set_instance_orlib",
-    "pm_orlib_closure", "pm_set_instance_dense",
+    "pm_orlib_closure", "pm_set_instance_dense", "pm_nccl_unique_id", "pm_nccl_create", "pm_nccl_destroy",
+    "pm_nccl_allgather",
 )
 
 
@@ -103,6 +104,54 @@ def ga_config(nb=60, nt=256, evolve_limit=100, saturation=10, seed=1, crossover_
                     -1 if mutation_iters is None else mutation_iters,
                     MIGRATE_TEAM if team else MIGRATE_BLOCK,
                     POPULATION_REFERENCE if population == "reference" else POPULATION_DEVICE)
+
+
+_lib.pm_nccl_unique_id.argtypes = [C.c_char_p]
+_lib.pm_nccl_create.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
+_lib.pm_nccl_destroy.argtypes = [_vp]
+_lib.pm_nccl_destroy.restype = None
+_lib.pm_nccl_allgather.argtypes = [_vp, _sz, _vp, _vp]
+_NCCL_ALLGATHER = ALLGATHER_FN(("pm_nccl_allgather", _lib))
+NCCL_ID_BYTES = 128
+
+
+def nccl_unique_id() -> bytes:
+    """pm_nccl_unique_id: rank 0 creates it, the launcher hands it to every rank."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    if _lib.pm_nccl_unique_id(buf) != 0:
+        raise NcclError("ncclGetUniqueId failed")
+    return buf.raw
+
+
+class NcclComm:
+    """The library's native island communicator (pm_nccl_create); pass it as
+    `allgather` to Context.run_ga."""
+
+    def __init__(self, unique_id: bytes, rank: int, world: int, device: int = 0):
+        h = _vp()
+        rc = _lib.pm_nccl_create(C.create_string_buffer(unique_id, NCCL_ID_BYTES), rank, world, device,
+                                 C.byref(h))
+        if rc != 0:
+            raise NcclError(f"pm_nccl_create failed ({rc})")
+        self._h = h
+        self.world = world
+
+    def allgather(self, data: bytes) -> bytes:
+        """One pm_nccl_allgather: every rank's `data` (equal sizes), in rank order."""
+        send = C.create_string_buffer(data, len(data))
+        recv = C.create_string_buffer(len(data) * self.world)
+        rc = _lib.pm_nccl_allgather(send, len(data), recv, self._h)
+        if rc != 0:
+            raise NcclError(f"pm_nccl_allgather failed ({rc})")
+        return recv.raw
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.pm_nccl_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 def torch_allgather(group=None, device=None):
@@ -358,6 +407,9 @@ class Context:
         r = _RunResult()
         if world == 1 and allgather is None:
             rc = _lib.pm_run_ga(self._h, C.byref(cfg), best.ctypes.data, per.ctypes.data, C.byref(r))
+        elif isinstance(allgather, NcclComm):  # the library's own NCCL exchange, no Python in the loop
+            rc = _lib.pm_run_ga_islands(self._h, C.byref(cfg), rank, world, _NCCL_ALLGATHER, allgather._h,
+                                        best.ctypes.data, per.ctypes.data, C.byref(r))
         else:
             cb = ALLGATHER_FN(allgather)
             rc = _lib.pm_run_ga_islands(self._h, C.byref(cfg), rank, world, cb, None, best.ctypes.data,

@@ -1,0 +1,83 @@
+// K4 native exchange: the island allgather of pm_run_ga_islands over NCCL
+// (one communicator per rank/GPU), for C/C++ hosts that do not run
+// torch.distributed.  Replaces the reference's in-process worker pool merge
+// (ga.cpp:253-282): every rank receives all block-best records and computes
+// the same global best.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+
+#include "../../include/pmedian_b200.h"
+
+struct pm_nccl {
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  unsigned char* dbuf = nullptr;  // world * bytes
+  size_t cap = 0;
+  int rank = 0, world = 1, device = 0;
+};
+
+static_assert(PM_NCCL_ID_BYTES == NCCL_UNIQUE_ID_BYTES, "NCCL unique id size");
+
+extern "C" {
+
+int pm_nccl_unique_id(char id[PM_NCCL_ID_BYTES]) {
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return PM_NCCL;
+  std::memcpy(id, u.internal, PM_NCCL_ID_BYTES);
+  return PM_OK;
+}
+
+int pm_nccl_create(const char id[PM_NCCL_ID_BYTES], int rank, int world, int device, pm_nccl** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return PM_DOMAIN;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return PM_CUDA;
+  pm_nccl* c = new pm_nccl;
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, PM_NCCL_ID_BYTES);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return PM_CUDA;
+  }
+  if (ncclCommInitRank(&c->comm, world, u, rank) != ncclSuccess) {
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return PM_NCCL;
+  }
+  *out = c;
+  return PM_OK;
+}
+
+void pm_nccl_destroy(pm_nccl* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->dbuf) cudaFree(c->dbuf);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int pm_nccl_allgather(const void* send, size_t bytes, void* recv, void* user) {
+  pm_nccl* c = static_cast<pm_nccl*>(user);
+  if (!c || (!send && bytes)) return PM_NCCL;
+  if (cudaSetDevice(c->device) != cudaSuccess) return PM_CUDA;
+  const size_t need = bytes * (size_t)c->world;
+  if (need > c->cap) {
+    if (c->dbuf) cudaFree(c->dbuf);
+    c->dbuf = nullptr;
+    c->cap = 0;
+    if (cudaMalloc(&c->dbuf, need) != cudaSuccess) return PM_CUDA;
+    c->cap = need;
+  }
+  unsigned char* mine = c->dbuf + bytes * (size_t)c->rank;  // in-place allgather
+  if (cudaMemcpyAsync(mine, send, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) return PM_CUDA;
+  if (ncclAllGather(mine, c->dbuf, bytes, ncclUint8, c->comm, c->stream) != ncclSuccess) return PM_NCCL;
+  if (cudaMemcpyAsync(recv, c->dbuf, need, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) return PM_CUDA;
+  return cudaStreamSynchronize(c->stream) == cudaSuccess ? PM_OK : PM_CUDA;
+}
+
+}  // extern "C"

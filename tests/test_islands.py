@@ -93,3 +93,25 @@ def test_islands_world_size_invariance():
         p.join(60)
     for rank, out in res:
         assert out == single, rank
+
+
+@pytest.mark.gpu
+def test_native_nccl_exchange_single_rank():
+    """pm_nccl_* (the library's own NCCL island exchange): a one-rank
+    communicator returns the record unchanged, and run_ga through it equals the
+    plain run.  (Several ranks need several GPUs; the rank-order contract is
+    the one the gloo test above checks for the torch adapter.)"""
+    import paper_1610_10061_b200 as pm
+    from paper_1610_10061_b200 import synth
+    comm = pm.NcclComm(pm.nccl_unique_id(), 0, 1, 0)
+    data = bytes(range(200)) * 3
+    assert comm.allgather(data) == data
+    ctx = pm.Context(0)
+    ctx.set_instance(synth.euclid_costs(300, 12345), 300, 300, 30)
+    cfg = pm.ga_config(nb=4, nt=32, evolve_limit=5, saturation=5, seed=3)
+    a = ctx.run_ga(cfg)
+    b = ctx.run_ga(cfg, rank=0, world=1, allgather=comm)
+    assert a["best_cost"] == b["best_cost"] and (a["best"] == b["best"]).all()
+    assert (a["per_kernel_best_costs"] == b["per_kernel_best_costs"]).all()
+    comm.close()
+    ctx.close()
