@@ -217,3 +217,21 @@ def test_evolve_blocks_paper_shape_matches_reference(ctx, pm, oracle, reflib):
             assert rc == 0
             assert (got[b * nt:(b + 1) * nt] == want).all(), (kernel, b)
             assert bc[b] == wcost and bt[b] == wthread, (kernel, b)
+
+
+@pytest.mark.parametrize("npts,p,nb,nt", [(3000, 300, 4, 64), (6000, 60, 2, 128)])
+def test_evolve_blocks_wide_chromosomes_match_reference(ctx, pm, reflib, npts, p, nb, nt):
+    """Crossover and shift mutations over 47- and 94-word chromosomes (large
+    exchange counts, multi-word rotations), block for block against the
+    reference's evolve_block."""
+    from paper_1610_10061_b200 import synth
+    costs = synth.euclid_costs(npts, 12345)
+    ctx.set_instance(costs, npts, npts, p)
+    ri = reflib.create(npts, npts, p, costs)
+    blocks = synth.random_population(npts, p, nb * nt, seed=5)
+    got, bc, bt = ctx.evolve_blocks(blocks, pm.ga_config(nb=nb, nt=nt, seed=2), 1)
+    for b in range(nb):
+        rc, want, _, wcost, wthread = ri.evolve_block(blocks[b * nt:(b + 1) * nt], nt, nb, 2, 1, b, -1, -1)
+        assert rc == 0
+        assert (got[b * nt:(b + 1) * nt] == want).all(), b
+        assert bc[b] == wcost and bt[b] == wthread, b
