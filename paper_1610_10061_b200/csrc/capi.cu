@@ -38,7 +38,9 @@ int pm_create(int device, pm_ctx** out) {
   }
   c->stream = c->own;
   if (c->errw.ensure(kErrSlots * 8) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->draw_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->draw_ev, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return PM_CUDA;
   }
@@ -65,6 +67,11 @@ void pm_destroy(pm_ctx* c) {
       cudaEventDestroy(e.second);
     }
   for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
+  if (c->draw_stream) {
+    cudaStreamSynchronize(c->draw_stream);
+    cudaStreamDestroy(c->draw_stream);
+  }
+  if (c->draw_ev) cudaEventDestroy(c->draw_ev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;

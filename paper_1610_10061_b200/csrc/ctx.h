@@ -103,6 +103,8 @@ struct pm_ctx {
   int open_cap = 0;
   GaBuffers ga;
   cudaStream_t copy_stream = nullptr;  // H2D of pipelined host-buffer calls
+  cudaStream_t draw_stream = nullptr;  // the GA's next-population draw, overlapped with evolution
+  cudaEvent_t draw_ev = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
 
   // kernel timing hook: events around the dominant evaluation kernel

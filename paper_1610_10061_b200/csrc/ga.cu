@@ -658,6 +658,10 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     PM_CUDA_TRY(c, B.rstate.ensure(24));  // {position (even gen), position (odd gen), shortfall}
     PM_CUDA_TRY(c, cudaMemsetAsync(B.rstate.p, 0, 24, c->stream));
   }
+  // Draws run on their own stream: the population of generation g+1 does not
+  // depend on generation g (ga.cpp:274), so its draw overlaps g's evolution;
+  // the main stream waits for it only before migrating into it.
+  cudaStream_t ds = c->draw_stream;
   auto draw = [&](DevBuf& dst, uint64_t generation) -> int {
     if (ref_draw && hd.L) {
       const int L = (int)hd.L, total = (int)(nb * nt);
@@ -670,24 +674,24 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
       uint32_t* blockcnt = flags + A;
       const int slot = (int)(generation & 1);
       const uint64_t* bound = B.table.as<uint64_t>() + (size_t)(s.p + 1) * s.m * L;
-      k_rank_flags<<<G, 256, 0, c->stream>>>(hd.stream.state, B.rstate.as<unsigned long long>(), slot, hd.words,
+      k_rank_flags<<<G, 256, 0, ds>>>(hd.stream.state, B.rstate.as<unsigned long long>(), slot, hd.words,
                                              hd.top_mask, bound, L, A, flags, blockcnt);
-      k_rank_compact<<<G, 256, 0, c->stream>>>(hd.stream.state, B.rstate.as<unsigned long long>(), slot, hd.words,
+      k_rank_compact<<<G, 256, 0, ds>>>(hd.stream.state, B.rstate.as<unsigned long long>(), slot, hd.words,
                                                hd.top_mask, L, A, flags, blockcnt, total, (int)(block0 * nt),
                                                (int)((block0 + nbl) * nt), B.ranks.as<uint64_t>());
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 2;
       const unsigned g = cdiv(count * 32, 256);
-      if (L <= 8) k_unrank<8><<<g, 256, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
-      else if (L <= 16) k_unrank<16><<<g, 256, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
-      else k_unrank<32><<<g, 256, 0, c->stream>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      if (L <= 8) k_unrank<8><<<g, 256, 0, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      else if (L <= 16) k_unrank<16><<<g, 256, 0, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      else k_unrank<32><<<g, 256, 0, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 1;
     } else if (ref_draw) {
       hd.draw(nb * nt, block0 * nt, (block0 + nbl) * nt, host_pop.data());
-      PM_CUDA_TRY(c, cudaMemcpyAsync(dst.p, host_pop.data(), count * wp * 8, cudaMemcpyHostToDevice, c->stream));
+      PM_CUDA_TRY(c, cudaMemcpyAsync(dst.p, host_pop.data(), count * wp * 8, cudaMemcpyHostToDevice, ds));
     } else {
-      k_draw_population<<<cdiv(count, 64), 64, 0, c->stream>>>(dst.as<uint64_t>(), (int)count, (int)wp, s.m,
+      k_draw_population<<<cdiv(count, 64), 64, 0, ds>>>(dst.as<uint64_t>(), (int)count, (int)wp, s.m,
                                                                   s.p, cfg->seed, generation, block0 * nt);
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 1;
@@ -696,8 +700,12 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
   };
   PM_CUDA_TRY(c, cudaMemsetAsync(c->errw.p, 0xff, 8, c->stream));
   PM_CUDA_TRY(c, cudaMemsetAsync(B.evals.p, 0, 8, c->stream));
+  PM_CUDA_TRY(c, cudaEventRecord(c->draw_ev, c->stream));  // table / rstate uploads above
+  PM_CUDA_TRY(c, cudaStreamWaitEvent(ds, c->draw_ev, 0));
   rc = draw(B.pop, 0);
   if (rc) return rc;
+  PM_CUDA_TRY(c, cudaEventRecord(c->draw_ev, ds));
+  PM_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->draw_ev, 0));
 
   // per-block record exchanged between islands: {cost, thread, words[wp]},
   // written by k_block_min and copied to pinned memory in one transfer
@@ -747,6 +755,8 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
       kernels = (size_t)kernel + 1;
       break;
     }
+    PM_CUDA_TRY(c, cudaEventRecord(c->draw_ev, ds));  // the next population is drawn
+    PM_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->draw_ev, 0));
     // migrate (ga.cpp:204-215) into the freshly drawn population: one
     // transfer from pinned staging (block b's best to slot 0 of block b, or
     // in team mode every block's best to slots 0..nb-1 of block 0)
@@ -760,6 +770,7 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     }
     std::swap(B.pop, B.next);
   }
+  PM_CUDA_TRY(c, cudaStreamSynchronize(ds));  // the last (unused) draw
   unsigned long long ref_evals = 0, rstate[3] = {0, 0, 0};
   PM_CUDA_TRY(c, cudaMemcpyAsync(&ref_evals, B.evals.p, 8, cudaMemcpyDeviceToHost, c->stream));
   if (ref_draw && hd.L)
