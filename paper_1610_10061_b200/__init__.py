@@ -288,6 +288,22 @@ class Context:
             if handle == 0:
                 handle = 1  # torch's default stream is the legacy NULL stream: cudaStreamLegacy
         self._check(_lib.pm_set_stream(self._h, handle))
+        self._stream_handle = handle
+
+    def _after_torch(self, *tensors) -> None:
+        """Device buffers written by torch on its current stream must be complete
+        before the context's stream reads them: nothing to do when the context
+        runs on that same stream (set_stream), else wait for it on the host
+        (the context's own stream is non-blocking, so it does not order against
+        torch's default stream by itself)."""
+        import torch
+        for t in tensors:
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                cur = torch.cuda.current_stream(t.device)
+                h = cur.cuda_stream or 1
+                if getattr(self, "_stream_handle", None) != h:
+                    cur.synchronize()
+                return
 
     def set_eval_kernel(self, kind: int) -> None:
         self._check(_lib.pm_set_eval_kernel(self._h, kind))
@@ -305,6 +321,7 @@ class Context:
         else:  # CUDA tensor of int64
             if costs.numel() != n * m:
                 raise StructuralError("cost matrix must be exactly n rows by m columns")
+            self._after_torch(costs)
             self._check(_lib.pm_set_instance_device(self._h, _ptr(costs), n, m, p))
         self.n, self.m, self.p = n, m, p
 
@@ -364,6 +381,7 @@ class Context:
         """CUDA buffers (torch tensors): words int64/uint64 [count, wp], costs_out int64 [count].
         check=False keeps the call asynchronous (errors via check_errors())."""
         fb = _sz(0)
+        self._after_torch(words)
         rc = _lib.pm_evaluate_device(self._h, _ptr(words), count, wp, _ptr(costs_out),
                                      C.byref(fb) if check else None)
         self._check(rc, fb.value)
@@ -374,6 +392,7 @@ class Context:
 
     def scan_depths_device(self, words, sum_k_out, count: int, wp: int) -> None:
         """sum_k_out[c] = sum_i k*_i (1-based stopping columns) for chromosome c."""
+        self._after_torch(words)
         self._check(_lib.pm_scan_depths_device(self._h, _ptr(words), count, wp, _ptr(sum_k_out)))
 
     def set_profiling(self, on: bool) -> None:

@@ -654,7 +654,11 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     const std::vector<uint64_t> tab = binomial_table(s.m, s.p, hd.L);
     PM_CUDA_TRY(c, B.table.ensure(tab.size() * 8));
     PM_CUDA_TRY(c, B.ranks.ensure(count * hd.L * 8));
-    PM_CUDA_TRY(c, cudaMemcpy(B.table.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+    // stream-ordered upload: a plain cudaMemcpy runs on the legacy stream, which
+    // does not order against the context's non-blocking streams (the first
+    // draw could read a partly written table)
+    PM_CUDA_TRY(c, cudaMemcpyAsync(B.table.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // `tab` is freed at the end of this block
     PM_CUDA_TRY(c, B.rstate.ensure(24));  // {position (even gen), position (odd gen), shortfall}
     PM_CUDA_TRY(c, cudaMemsetAsync(B.rstate.p, 0, 24, c->stream));
   }
