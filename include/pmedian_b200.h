@@ -68,7 +68,11 @@ int pm_create(int device, pm_ctx** out);
 void pm_destroy(pm_ctx* ctx);
 /* Text of the last failure on this context ("" if none).  Valid until the next call. */
 const char* pm_last_error(const pm_ctx* ctx);
-/* Routes all later work to `stream` (a cudaStream_t; NULL restores the context's own). */
+/* Routes all later work to `stream` (a cudaStream_t; NULL restores the context's own).
+ * Device buffers passed to the *_device entry points are read in order on this
+ * stream: a producer on another stream must be complete (or joined with an
+ * event) first.  The context's own stream is non-blocking, i.e. it does not
+ * order against the legacy default stream. */
 int pm_set_stream(pm_ctx* ctx, void* stream);
 /* Number of kernels this context has launched so far (evidence counter for bench/tests). */
 uint64_t pm_kernel_launches(const pm_ctx* ctx);
