@@ -117,6 +117,55 @@ class Tables {
     return evaluate_population(words, 1)[0];
   }
 
+  // evolve_block (ga.cpp:136-194) over nb consecutive blocks of cfg.nt
+  // chromosomes, in place; block b is global block first_block + b.
+  struct BlockResult {
+    std::int64_t best_cost;
+    std::size_t best_thread;
+  };
+  std::vector<BlockResult> evolve_blocks(std::vector<std::uint64_t>& blocks, std::size_t nb,
+                                         const pm_ga_config& cfg, std::uint64_t kernel_index,
+                                         std::size_t first_block = 0) {
+    std::vector<std::int64_t> bc(nb);
+    std::vector<std::size_t> bt(nb);
+    const std::size_t wp = nb ? blocks.size() / (nb * cfg.nt) : 0;
+    check(pm_evolve_blocks(ctx_, blocks.data(), nb, wp, &cfg, kernel_index, first_block, bc.data(), bt.data()));
+    std::vector<BlockResult> out(nb);
+    for (std::size_t b = 0; b < nb; ++b) out[b] = {bc[b], bt[b]};
+    return out;
+  }
+
+  // run_ga (ga.cpp:219-303): RunResult plus work counters.  With world > 1,
+  // this rank's islands exchange block bests through `allgather` (e.g.
+  // pm_nccl_allgather with a NcclIslands communicator as `user`).
+  struct RunResult {
+    std::vector<std::uint64_t> best;
+    std::int64_t best_cost = 0;
+    std::size_t kernels_executed = 0, kernel_of_best = 0;
+    std::vector<std::int64_t> per_kernel_best_costs;
+    double wall_time = 0;
+    std::uint64_t evaluations = 0;
+  };
+  RunResult run_ga(const pm_ga_config& cfg, int rank = 0, int world = 1, pm_allgather_fn allgather = nullptr,
+                   void* user = nullptr) {
+    const pm_table_info ti = info();
+    RunResult r;
+    r.best.assign((ti.sites + 63) / 64, 0);
+    r.per_kernel_best_costs.assign(cfg.evolve_limit, 0);
+    pm_run_result res{};
+    check(world == 1 && !allgather
+              ? pm_run_ga(ctx_, &cfg, r.best.data(), r.per_kernel_best_costs.data(), &res)
+              : pm_run_ga_islands(ctx_, &cfg, rank, world, allgather, user, r.best.data(),
+                                  r.per_kernel_best_costs.data(), &res));
+    r.best_cost = res.best_cost;
+    r.kernels_executed = res.kernels_executed;
+    r.kernel_of_best = res.kernel_of_best;
+    r.per_kernel_best_costs.resize(res.kernels_executed);
+    r.wall_time = res.wall_time_s;
+    r.evaluations = res.evaluations;
+    return r;
+  }
+
   std::vector<std::int64_t> min_cost_sum(const std::vector<std::uint64_t>& words, std::size_t count) const {
     std::vector<std::int64_t> out(count);
     if (count == 0) return out;
@@ -131,6 +180,44 @@ class Tables {
     if (rc != PM_OK) throw_status(rc, pm_last_error(ctx_));
   }
   pm_ctx* ctx_ = nullptr;
+};
+
+// The default GaConfig (ga.hpp:24-38) in the C ABI's form.
+inline pm_ga_config ga_config(std::size_t nb = 60, std::size_t nt = 256, std::size_t evolve_limit = 100,
+                              std::size_t saturation = 10, std::uint64_t seed = 1) {
+  pm_ga_config c{};
+  c.nb = nb;
+  c.nt = nt;
+  c.evolve_limit = evolve_limit;
+  c.saturation = saturation;
+  c.seed = seed;
+  c.crossover_iters = -1;
+  c.mutation_iters = -1;
+  c.migration = PM_MIGRATE_BLOCK;
+  c.population = PM_POPULATION_REFERENCE;
+  return c;
+}
+
+// One NCCL communicator per rank for the island exchange; pass
+// (pm_nccl_allgather, islands.comm()) to Tables::run_ga.
+class NcclIslands {
+ public:
+  static std::string unique_id() {
+    std::string id(PM_NCCL_ID_BYTES, '\0');
+    if (pm_nccl_unique_id(id.data()) != PM_OK) throw DeviceError("ncclGetUniqueId failed");
+    return id;
+  }
+  NcclIslands(const std::string& id, int rank, int world, int device) {
+    const int rc = pm_nccl_create(id.data(), rank, world, device, &comm_);
+    if (rc != PM_OK) throw_status(rc, "pm_nccl_create failed");
+  }
+  NcclIslands(const NcclIslands&) = delete;
+  NcclIslands& operator=(const NcclIslands&) = delete;
+  ~NcclIslands() { pm_nccl_destroy(comm_); }
+  pm_nccl* comm() const { return comm_; }
+
+ private:
+  pm_nccl* comm_ = nullptr;
 };
 
 }  // namespace b200

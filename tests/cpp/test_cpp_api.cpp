@@ -63,6 +63,26 @@ int main() {
     threw = std::string(e.what()) == "p must be < m";
   }
   EXPECT(threw);
+  // run_ga on Example 1 (test_ga.cpp:322-336): optimum 35 at 1001, every seed
+  for (std::uint64_t seed = 1; seed <= 5; ++seed) {
+    const auto r = t.run_ga(pmedian::b200::ga_config(2, 4, 10, 10, seed));
+    EXPECT(r.best_cost == 35 && r.best == bits("1001"));
+    EXPECT(r.per_kernel_best_costs.size() == r.kernels_executed);
+  }
+  // the same run through the library's NCCL island exchange (one rank)
+  {
+    pmedian::b200::NcclIslands isl(pmedian::b200::NcclIslands::unique_id(), 0, 1, 0);
+    const auto a = t.run_ga(pmedian::b200::ga_config(2, 4, 10, 10, 7));
+    const auto b = t.run_ga(pmedian::b200::ga_config(2, 4, 10, 10, 7), 0, 1, pm_nccl_allgather, isl.comm());
+    EXPECT(a.best_cost == b.best_cost && a.per_kernel_best_costs == b.per_kernel_best_costs);
+  }
+  // evolve_block keeps an optimal chromosome (test_ga.cpp:224-244)
+  {
+    std::vector<std::uint64_t> blk;
+    for (int i = 0; i < 4; ++i) blk.push_back(bits("1001")[0]);
+    const auto br = t.evolve_blocks(blk, 1, pmedian::b200::ga_config(1, 4), 0);
+    EXPECT(br.size() == 1 && br[0].best_cost == 35);
+  }
   std::printf("%s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
   return failures ? 1 : 0;
 }
