@@ -16,7 +16,7 @@ build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) includ
 	$(NVCC) $(NVFLAGS) -Xptxas -warn-spills -c $< -o $@
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lnccl -lrt -ldl -lpthread
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lrt -ldl -lpthread
 
 # the reference CLI over the device path (host code; nvcc for the shared headers)
 $(CLI): $(PKG)/cli/pmedian_bench.cpp $(LIB) $(PKG)/csrc/combinatorics.h

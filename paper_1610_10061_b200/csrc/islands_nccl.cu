@@ -3,10 +3,17 @@
 // torch.distributed.  Replaces the reference's in-process worker pool merge
 // (ga.cpp:253-282): every rank receives all block-best records and computes
 // the same global best.
+//
+// NCCL is bound at run time (dlopen on first use), not linked: a process that
+// loads this library before PyTorch would otherwise pin the system libnccl.so.2
+// and torch's own (newer) NCCL could no longer resolve its symbols.  If a
+// libnccl.so.2 is already loaded (e.g. torch's), that one is used.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstring>
+#include <mutex>
 
 #include "../../include/pmedian_b200.h"
 
@@ -20,11 +27,41 @@ struct pm_nccl {
 
 static_assert(PM_NCCL_ID_BYTES == NCCL_UNIQUE_ID_BYTES, "NCCL unique id size");
 
+namespace {
+
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_gather;
+  });
+  return api;
+}
+
+}  // namespace
+
 extern "C" {
 
 int pm_nccl_unique_id(char id[PM_NCCL_ID_BYTES]) {
+  if (!nccl().ok) return PM_NCCL;
   ncclUniqueId u;
-  if (ncclGetUniqueId(&u) != ncclSuccess) return PM_NCCL;
+  if (nccl().get_unique_id(&u) != ncclSuccess) return PM_NCCL;
   std::memcpy(id, u.internal, PM_NCCL_ID_BYTES);
   return PM_OK;
 }
@@ -32,6 +69,7 @@ int pm_nccl_unique_id(char id[PM_NCCL_ID_BYTES]) {
 int pm_nccl_create(const char id[PM_NCCL_ID_BYTES], int rank, int world, int device, pm_nccl** out) {
   if (!out || world < 1 || rank < 0 || rank >= world) return PM_DOMAIN;
   *out = nullptr;
+  if (!nccl().ok) return PM_NCCL;
   if (cudaSetDevice(device) != cudaSuccess) return PM_CUDA;
   pm_nccl* c = new pm_nccl;
   c->rank = rank;
@@ -43,7 +81,7 @@ int pm_nccl_create(const char id[PM_NCCL_ID_BYTES], int rank, int world, int dev
     delete c;
     return PM_CUDA;
   }
-  if (ncclCommInitRank(&c->comm, world, u, rank) != ncclSuccess) {
+  if (nccl().comm_init_rank(&c->comm, world, u, rank) != ncclSuccess) {
     cudaStreamDestroy(c->stream);
     delete c;
     return PM_NCCL;
@@ -55,7 +93,7 @@ int pm_nccl_create(const char id[PM_NCCL_ID_BYTES], int rank, int world, int dev
 void pm_nccl_destroy(pm_nccl* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm) nccl().comm_destroy(c->comm);
   if (c->dbuf) cudaFree(c->dbuf);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -75,7 +113,7 @@ int pm_nccl_allgather(const void* send, size_t bytes, void* recv, void* user) {
   }
   unsigned char* mine = c->dbuf + bytes * (size_t)c->rank;  // in-place allgather
   if (cudaMemcpyAsync(mine, send, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) return PM_CUDA;
-  if (ncclAllGather(mine, c->dbuf, bytes, ncclUint8, c->comm, c->stream) != ncclSuccess) return PM_NCCL;
+  if (nccl().all_gather(mine, c->dbuf, bytes, ncclUint8, c->comm, c->stream) != ncclSuccess) return PM_NCCL;
   if (cudaMemcpyAsync(recv, c->dbuf, need, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) return PM_CUDA;
   return cudaStreamSynchronize(c->stream) == cudaSuccess ? PM_OK : PM_CUDA;
 }

@@ -43,3 +43,19 @@ def test_error_taxonomy_matches_reference(pm):
     assert issubclass(pm.DomainError, ValueError)
     assert pm.StructuralError.status == 1 and pm.ContractError.status == 2
     assert pm.DomainError.status == 3 and pm.BudgetError.status == 4
+
+
+def test_library_does_not_pin_nccl_before_torch(pm):
+    """The library binds NCCL at run time (islands_nccl.cu): loading it before
+    PyTorch must not pin the system libnccl.so.2 under torch's own NCCL."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", "import paper_1610_10061_b200, torch; print(torch.__version__)"],
+                       cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    with open(pm.LIB_PATH, "rb") as f:
+        assert b"libnccl.so.2\x00" in f.read()  # the dlopen name, not a DT_NEEDED entry
+    needed = subprocess.run(["readelf", "-d", pm.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libnccl" not in needed

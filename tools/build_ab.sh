@@ -11,4 +11,4 @@ F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -
 nvcc $F -c paper_1610_10061_b200/csrc/fitness_ab.cu -o build_ab/fitness.o
 others=$(ls build/*.o | grep -v '/fitness.o$')
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_1610_10061_b200/libpmedian_b200_ab.so \
-  $others build_ab/fitness.o -lcudart_static -lnccl -lrt -ldl -lpthread
+  $others build_ab/fitness.o -lcudart_static -lrt -ldl -lpthread
