@@ -205,7 +205,22 @@ __global__ void __launch_bounds__(512, 1)
           uint4* dstT = reinterpret_cast<uint4*>(Tsm);
           for (size_t x = tid; x < Ts / 2; x += blockDim.x) dstT[x] = src[x];
         } else {
-          for (size_t x = tid; x < Ts; x += blockDim.x) Tsm[x] = (MaskT)(Tg[x] >> half);
+          // 8 independent loads in flight per thread: small CTAs (2 warps at
+          // pmed40's shape) would otherwise pay one L2 round trip per 64 masks
+          constexpr int kU = 8;
+          for (size_t x0 = tid; x0 < Ts; x0 += (size_t)blockDim.x * kU) {
+            uint64_t v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const size_t x = x0 + (size_t)u * blockDim.x;
+              v[u] = x < Ts ? __ldg(Tg + x) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const size_t x = x0 + (size_t)u * blockDim.x;
+              if (x < Ts) Tsm[x] = (MaskT)(v[u] >> half);
+            }
+          }
         }
       }
       for (int x = tid; x < nwarps * kG * 32; x += blockDim.x) acc[x] = 0;

@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 #include <limits>
@@ -209,63 +211,76 @@ __global__ void k_popcount_check(const uint64_t* __restrict__ pop, int count, in
 // ~p dependent probes instead of ~m.  The table is limb-major ([y][limb][x]),
 // so each limb load of a probe is one contiguous 256-byte run.  Same subsets as the reference's walk,
 // bit for bit (tests/test_gpu_ga.py).
-// One probe of 32 consecutive candidates with kN-limb arithmetic (X and the
-// probed binomials fit in kN limbs at this step); on a hit, X -= C(a-j, k+1)
-// and the lane index of the taken candidate is returned, else -1.
-template <int kN, int kL>
-__device__ __forceinline__ int unrank_probe(const uint64_t* __restrict__ table, int m, int L, int k, int x,
-                                            uint64_t (&X)[kL]) {
+// One probe of S consecutive candidates per chromosome with kN-limb
+// arithmetic (X and the probed binomials fit in kN limbs at this step).  The
+// warp holds 32/S chromosomes, one S-lane group each; every lane of the warp
+// runs the probe (`live` false for a finished group), so the warp stays
+// converged.  On a hit the group's X -= C(a-j, k+1) and `jl` is the lane (in
+// the group) of the taken candidate.
+template <int kN, int kL, int S>
+__device__ __forceinline__ bool unrank_probe(const uint64_t* __restrict__ table, int m, int L, int k, int x,
+                                             bool live, int gbase, uint64_t (&X)[kL], int& jl) {
   uint64_t cv[kN];
-  int cmp = -1;  // sign of C(x, k+1) - X; C(x, .) = 0 for x < 0
-  if (x >= 0) {
-    const uint64_t* cp = table + (size_t)(k + 1) * L * m + x;  // limb i at cp[i * m]
+  int cmp = 1;  // sign of C(x, k+1) - X; C(x, .) = 0 for x < 0
+  if (live) {
+    cmp = -1;
+    if (x >= 0) {
+      const uint64_t* cp = table + (size_t)(k + 1) * L * m + x;  // limb i at cp[i * m]
 #pragma unroll
-    for (int i = 0; i < kN; ++i) cv[i] = i < L ? __ldg(cp + (size_t)i * m) : 0;  // bucket may exceed L
-    cmp = 0;
+      for (int i = 0; i < kN; ++i) cv[i] = i < L ? __ldg(cp + (size_t)i * m) : 0;  // bucket may exceed L
+      cmp = 0;
 #pragma unroll
-    for (int i = kN - 1; i >= 0; --i)
-      if (cmp == 0) cmp = cv[i] < X[i] ? -1 : (cv[i] > X[i] ? 1 : 0);
+      for (int i = kN - 1; i >= 0; --i)
+        if (cmp == 0) cmp = cv[i] < X[i] ? -1 : (cv[i] > X[i] ? 1 : 0);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kN; ++i) cv[i] = 0;
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < kN; ++i) cv[i] = 0;
   }
-  const unsigned hit = __ballot_sync(kFull, cmp < 0);
-  if (!hit) return -1;
-  const int jl = __ffs(hit) - 1;
+  const unsigned bal = __ballot_sync(kFull, cmp < 0);
+  const unsigned hit = S == 32 ? bal : (bal >> gbase) & ((1u << S) - 1);
+  jl = hit ? __ffs(hit) - 1 : 0;
+  const bool take = live && hit != 0;
   uint64_t borrow = 0;
 #pragma unroll
   for (int i = 0; i < kN; ++i) {
-    const uint64_t v = __shfl_sync(kFull, cv[i], jl);
+    const uint64_t v = __shfl_sync(kFull, cv[i], gbase + jl);
     const uint64_t d = X[i] - v - borrow;
-    borrow = (X[i] < v) || (X[i] - v < borrow);
-    X[i] = d;
+    const uint64_t nb = (X[i] < v) || (X[i] - v < borrow);
+    if (take) {
+      X[i] = d;
+      borrow = nb;
+    }
   }
-  return jl;
+  return take;
 }
 
-// Dispatch on the step's limb count (warp-uniform): the smallest instantiated
-// width that holds it.
-template <int kL>
-__device__ __forceinline__ int unrank_probe_n(int lim, const uint64_t* __restrict__ table, int m, int L, int k,
-                                              int x, uint64_t (&X)[kL]) {
-  if (lim <= 1) return unrank_probe<1, kL>(table, m, L, k, x, X);
-  if (lim <= 2) return unrank_probe<2, kL>(table, m, L, k, x, X);
+// Dispatch on the step's limb count (warp-uniform: the largest over the
+// warp's groups): the smallest instantiated width that holds it.
+template <int kL, int S>
+__device__ __forceinline__ bool unrank_probe_n(int lim, const uint64_t* __restrict__ table, int m, int L, int k,
+                                               int x, bool live, int gbase, uint64_t (&X)[kL], int& jl) {
+  if (lim <= 1) return unrank_probe<1, kL, S>(table, m, L, k, x, live, gbase, X, jl);
+  if (lim <= 2) return unrank_probe<2, kL, S>(table, m, L, k, x, live, gbase, X, jl);
   if constexpr (kL >= 4) {
-    if (lim <= 3) return unrank_probe<3, kL>(table, m, L, k, x, X);
-    if (lim <= 4) return unrank_probe<4, kL>(table, m, L, k, x, X);
+    if (lim <= 3) return unrank_probe<3, kL, S>(table, m, L, k, x, live, gbase, X, jl);
+    if (lim <= 4) return unrank_probe<4, kL, S>(table, m, L, k, x, live, gbase, X, jl);
   }
   if constexpr (kL >= 8) {
-    if (lim <= 6) return unrank_probe<6, kL>(table, m, L, k, x, X);
-    if (lim <= 8) return unrank_probe<8, kL>(table, m, L, k, x, X);
+    if (lim <= 6) return unrank_probe<6, kL, S>(table, m, L, k, x, live, gbase, X, jl);
+    if (lim <= 8) return unrank_probe<8, kL, S>(table, m, L, k, x, live, gbase, X, jl);
   }
   if constexpr (kL >= 16) {
-    if (lim <= 12) return unrank_probe<12, kL>(table, m, L, k, x, X);
-    if (lim <= 16) return unrank_probe<16, kL>(table, m, L, k, x, X);
+    if (lim <= 12) return unrank_probe<12, kL, S>(table, m, L, k, x, live, gbase, X, jl);
+    if (lim <= 16) return unrank_probe<16, kL, S>(table, m, L, k, x, live, gbase, X, jl);
   }
   if constexpr (kL >= 32) {
-    if (lim <= 24) return unrank_probe<24, kL>(table, m, L, k, x, X);
+    if (lim <= 24) return unrank_probe<24, kL, S>(table, m, L, k, x, live, gbase, X, jl);
   }
-  return unrank_probe<kL, kL>(table, m, L, k, x, X);
+  return unrank_probe<kL, kL, S>(table, m, L, k, x, live, gbase, X, jl);
 }
 
 // Reference-exact unranking on the device (combinatorics.cpp:20-52): the
@@ -274,26 +289,30 @@ __device__ __forceinline__ int unrank_probe_n(int lim, const uint64_t* __restric
 // r -= C(a, k)); a run of skips telescopes (hockey stick:
 // sum_{t<j} C(a-t, k) = C(a+1, k+1) - C(a-j+1, k+1)), so with X = C(a+1, k+1) - r
 // the next taken candidate is the first j with C(a-j, k+1) < X, after which
-// X -= C(a-j, k+1), a -= j+1, k -= 1.  One warp per chromosome tests 32
-// consecutive candidates per probe (one contiguous table run per limb), so a
-// draw costs ~p dependent probes instead of ~m, each with only the limbs the
-// step's values need (X < C(m, k+1) shrinks as k falls).  Same subsets as the
-// reference's walk, bit for bit (tests/test_gpu_ga.py).
-template <int kL>
+// X -= C(a-j, k+1), a -= j+1, k -= 1.  A group of S lanes per chromosome tests
+// S consecutive candidates per probe (one contiguous table run per limb), so
+// a draw costs ~p * E[probes per gap] dependent probes instead of ~m, each
+// with only the limbs the step's values need (X < C(m, k+1) shrinks as k
+// falls).  S is picked from the gap density p/m (pick_unrank_group): 32 lanes
+// on one chromosome waste most of a probe when the mean gap m/p is ~10.
+// Same subsets as the reference's walk, bit for bit (tests/test_gpu_ga.py).
+template <int kL, int S>
 __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ranks,
                                                 const uint64_t* __restrict__ table, int m, int p, int L, int wp,
                                                 int count, uint64_t* __restrict__ out) {
-  const int idx = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (idx >= count) return;  // warp-uniform
+  const int gbase = S == 32 ? 0 : lane / S * S, gl = lane - gbase;
+  const int idx = (int)(((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5) * (32 / S) + lane / S);
+  const bool active = idx < count;
+  if (__ballot_sync(kFull, active) == 0) return;  // warp-uniform
   const uint64_t* bound = table + (size_t)(p + 1) * L * m;
   const uint64_t* lims = bound + L;  // limbs of C(m, k + 1), k < p
-  uint64_t X[kL];  // X = C(m, p) - r (every lane holds the same value)
+  uint64_t X[kL];  // X = C(m, p) - r (every lane of the group holds the same value)
   {
     uint64_t borrow = 0;
 #pragma unroll
     for (int i = 0; i < kL; ++i) {
-      if (i < L) {
+      if (active && i < L) {
         const uint64_t b = __ldg(bound + i), r = __ldg(ranks + (size_t)idx * L + i);
         X[i] = b - r - borrow;
         borrow = (b < r) || (b - r < borrow);
@@ -303,32 +322,69 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
     }
   }
   uint64_t* w = out + (size_t)idx * wp;
-  for (int i = lane; i < wp; i += 32) w[i] = 0;
+  if (active)
+    for (int i = gl; i < wp; i += S) w[i] = 0;
   __syncwarp();
-  int a = m - 1, k = p - 1, base = 0;
+  int a = m - 1, k = active ? p - 1 : -1, base = 0;
   int word_idx = 0;
   uint64_t word = 0;  // the output word being filled (candidates increase)
-  int lim = (int)__ldg(lims + k);
-  while (k >= 0) {
-    const int jl = unrank_probe_n<kL>(lim, table, m, L, k, a - base - lane, X);
-    if (jl < 0) {
-      base += 32;
-      continue;
+  int lim = k >= 0 ? (int)__ldg(lims + k) : 0;
+  while (true) {
+    const bool live = k >= 0;
+    if (__ballot_sync(kFull, live) == 0) break;
+    const int limw = __reduce_max_sync(kFull, live ? lim : 0);
+    int jl;
+    const bool take = unrank_probe_n<kL, S>(limw, table, m, L, k, a - base - gl, live, gbase, X, jl);
+    if (live) {
+      if (!take) {
+        base += S;
+      } else {
+        const int j = base + jl;
+        const int cand = m - 1 - a + j;
+        if ((cand >> 6) != word_idx) {
+          if (gl == 0 && word) w[word_idx] = word;
+          word_idx = cand >> 6;
+          word = 0;
+        }
+        word |= 1ull << (cand & 63);
+        a -= j + 1;
+        --k;
+        base = 0;
+        if (k >= 0) lim = (int)__ldg(lims + k);
+      }
     }
-    const int j = base + jl;
-    const int cand = m - 1 - a + j;
-    if ((cand >> 6) != word_idx) {
-      if (lane == 0 && word) w[word_idx] = word;
-      word_idx = cand >> 6;
-      word = 0;
-    }
-    word |= 1ull << (cand & 63);
-    a -= j + 1;
-    --k;
-    base = 0;
-    if (k >= 0) lim = (int)__ldg(lims + k);
   }
-  if (lane == 0 && word) w[word_idx] = word;
+  if (active && gl == 0 && word) w[word_idx] = word;
+}
+
+// Lanes per chromosome for k_unrank: the width S minimising the expected warp
+// work per draw, (S/32) * E[probes per gap] = (S/32) / (1 - (1 - p/m)^S)
+// (PMB_UNRANK_S overrides, for tuning).
+static int pick_unrank_group(int m, int p) {
+  if (const char* e = getenv("PMB_UNRANK_S")) {
+    const int s = atoi(e);
+    if (s == 8 || s == 16 || s == 32) return s;
+  }
+  const double q = (double)p / m;
+  int best = 32;
+  double bc = 1e300;
+  for (int s : {8, 16, 32}) {
+    const double c = s / 32.0 / (1.0 - std::pow(1.0 - q, s));
+    if (c < bc) {
+      bc = c;
+      best = s;
+    }
+  }
+  return best;
+}
+
+template <int kL>
+static void launch_unrank(int S, const uint64_t* ranks, const uint64_t* table, int m, int p, int L, int wp,
+                          int count, uint64_t* out, cudaStream_t st) {
+  const unsigned g = (unsigned)(((size_t)count * S + 255) / 256);
+  if (S == 8) k_unrank<kL, 8><<<g, 256, 0, st>>>(ranks, table, m, p, L, wp, count, out);
+  else if (S == 16) k_unrank<kL, 16><<<g, 256, 0, st>>>(ranks, table, m, p, L, wp, count, out);
+  else k_unrank<kL, 32><<<g, 256, 0, st>>>(ranks, table, m, p, L, wp, count, out);
 }
 
 // Reference-exact rank draws on the device.  The reference draws every rank of
@@ -685,10 +741,10 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
                                                (int)((block0 + nbl) * nt), B.ranks.as<uint64_t>());
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 2;
-      const unsigned g = cdiv(count * 32, 256);
-      if (L <= 8) k_unrank<8><<<g, 256, 0, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
-      else if (L <= 16) k_unrank<16><<<g, 256, 0, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
-      else k_unrank<32><<<g, 256, 0, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>());
+      const int S = pick_unrank_group(s.m, s.p);
+      if (L <= 8) launch_unrank<8>(S, B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>(), ds);
+      else if (L <= 16) launch_unrank<16>(S, B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>(), ds);
+      else launch_unrank<32>(S, B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>(), ds);
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 1;
     } else if (ref_draw) {
