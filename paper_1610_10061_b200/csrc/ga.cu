@@ -91,6 +91,42 @@ __global__ void k_mutation_children(const uint64_t* __restrict__ pop, uint64_t* 
     random_shift_mutation(parent, child + ((size_t)idx * attempts + a) * wp, m, rng);
 }
 
+// 32 chromosomes per 256-thread block: warp 0 draws every attempt's shift
+// (one keyed stream per chromosome, consumed in the reference's order), then
+// the whole block builds the children word by word -- attempts x words
+// independent outputs per chromosome, written coalesced.  (One thread per
+// chromosome left the kernel latency-bound: 15,360 threads at the paper's
+// shape is ~3 warps per SM.)
+__global__ void __launch_bounds__(256) k_mutation_children_wide(const uint64_t* __restrict__ pop,
+                                                                uint64_t* __restrict__ child, int nbl, int nt,
+                                                                int wp, int m, uint64_t seed, uint64_t kernel,
+                                                                uint64_t block0, int attempts) {
+  extern __shared__ ShiftDraw sd[];  // [32][attempts]
+  const int count = nbl * nt;
+  const int c0 = blockIdx.x * 32;
+  if (threadIdx.x < 32) {
+    const int idx = c0 + threadIdx.x;
+    if (idx < count) {
+      const int b = idx / nt, t = idx % nt;
+      const uint64_t key[4] = {kMutationTag, kernel, block0 + b, (uint64_t)t};
+      Stream rng = Stream::derive(seed, key, 4);
+      for (int a = 0; a < attempts; ++a) sd[threadIdx.x * attempts + a] = draw_shift(m, rng);
+    }
+  }
+  __syncthreads();
+  const int nc = min(32, count - c0);
+  const int per = attempts * wp;
+  const int total = nc * per;
+  const uint64_t* base = pop + (size_t)c0 * wp;
+  uint64_t* out = child + (size_t)c0 * per;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int cl = e / per, r = e - cl * per;
+    const int a = r / wp, wi = r - a * wp;
+    const ShiftDraw d = sd[cl * attempts + a];
+    out[e] = rotate_word(base + (size_t)cl * wp, d.lo, d.len, d.offset, wi);
+  }
+}
+
 __global__ void k_mutation_accept(uint64_t* __restrict__ pop, int64_t* __restrict__ cost,
                                   const uint64_t* __restrict__ child, const int64_t* __restrict__ ccost,
                                   int count, int attempts, int wp, unsigned long long* __restrict__ evals) {
@@ -515,9 +551,15 @@ static int evolve_all(pm_ctx* c, GaBuffers& B, const GaShape& s, uint64_t kernel
     }
   }
   if (s.attempts > 0) {
-    k_mutation_children<<<cdiv(count, tb), tb, 0, c->stream>>>(pop, B.child.as<uint64_t>(), s.nbl, s.nt,
-                                                                s.wp, s.m, s.seed, kernel, s.block0,
-                                                                s.attempts);
+    const size_t sd_bytes = (size_t)32 * s.attempts * sizeof(ShiftDraw);
+    if (sd_bytes <= 48 * 1024 && (size_t)s.attempts * s.wp * 32 < (size_t)INT32_MAX) {
+      k_mutation_children_wide<<<cdiv(count, 32), 256, sd_bytes, c->stream>>>(
+          pop, B.child.as<uint64_t>(), s.nbl, s.nt, s.wp, s.m, s.seed, kernel, s.block0, s.attempts);
+    } else {
+      k_mutation_children<<<cdiv(count, tb), tb, 0, c->stream>>>(pop, B.child.as<uint64_t>(), s.nbl, s.nt,
+                                                                  s.wp, s.m, s.seed, kernel, s.block0,
+                                                                  s.attempts);
+    }
     PM_CUDA_TRY(c, cudaGetLastError());
     rc = evaluate_core(c, B.child.as<uint64_t>(), count * s.attempts, B.ccost.as<int64_t>(), 0);
     if (rc) return rc;

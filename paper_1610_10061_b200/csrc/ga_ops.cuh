@@ -35,10 +35,29 @@ struct Stream {
   }
   __host__ __device__ uint64_t below(uint64_t bound) {
     if ((bound & (bound - 1)) == 0) return next() & (bound - 1);
+#ifdef __CUDA_ARCH__
+    if (bound < 65536) {  // the GA's bounds (m, p/2, span lengths): 32-bit remainders only
+      const uint32_t d = (uint32_t)bound;
+      const uint32_t t32 = (0xffffffffu % d + 1) % d;  // 2^32 mod d
+      const uint64_t threshold = (t32 * t32) % d;      // 2^64 mod d == (0 - bound) % bound
+      uint64_t v = next();
+      while (v < threshold) v = next();
+      return mod_small(v, d);
+    }
+#endif
     const uint64_t threshold = (0 - bound) % bound;
     uint64_t v = next();
     while (v < threshold) v = next();
     return v % bound;
+  }
+  // v mod d for d < 2^16 in 16-bit long-division steps (each a 32-bit remainder;
+  // a 64-bit remainder is a long software sequence on the GPU)
+  __host__ __device__ static uint64_t mod_small(uint64_t v, uint32_t d) {
+    uint32_t r = (uint32_t)(v >> 48) % d;
+    r = ((r << 16) | (uint32_t)((v >> 32) & 0xffffu)) % d;
+    r = ((r << 16) | (uint32_t)((v >> 16) & 0xffffu)) % d;
+    r = ((r << 16) | (uint32_t)(v & 0xffffu)) % d;
+    return r;
   }
   __host__ __device__ bool coin() { return (next() & 1) != 0; }
 };
@@ -68,38 +87,45 @@ __device__ __forceinline__ uint64_t extract_cyclic(const uint64_t* w, int base, 
   return extract_linear(w, base + r, first) | (extract_linear(w, base, cnt - first) << first);
 }
 
-// out[lo + (t + offset) % len] = in[lo + t] for t < len; other bits copied.
-// circular_shift is the case lo = 0, len = m (ga.cpp:65-75); block_shift the
-// general one (ga.cpp:77-90).  `offset` is already reduced to [0, len).
-__device__ void rotate_range(const uint64_t* in, uint64_t* out, int m, int lo, int len, int offset) {
-  const int wp = (m + 63) >> 6;
+// Word wi of out, where out[lo + (t + offset) % len] = in[lo + t] for t < len
+// and every other bit is copied.  circular_shift is the case lo = 0, len = m
+// (ga.cpp:65-75); block_shift the general one (ga.cpp:77-90).  `offset` is
+// already reduced to [0, len).
+__device__ __forceinline__ uint64_t rotate_word(const uint64_t* in, int lo, int len, int offset, int wi) {
+  uint64_t v = in[wi];
   const int hi = lo + len - 1;
-  for (int wi = 0; wi < wp; ++wi) {
-    uint64_t v = in[wi];
-    const int q0 = max(wi * 64, lo), q1 = min(wi * 64 + 63, hi);
-    if (q0 <= q1 && offset != 0) {
-      const int cnt = q1 - q0 + 1;
-      int r = (q0 - lo - offset) % len;
-      if (r < 0) r += len;
-      const uint64_t bits = extract_cyclic(in, lo, len, r, cnt);
-      const int sh = q0 - wi * 64;
-      const uint64_t mask = low_mask(cnt) << sh;
-      v = (v & ~mask) | ((bits << sh) & mask);
-    }
-    out[wi] = v;
+  const int q0 = max(wi * 64, lo), q1 = min(wi * 64 + 63, hi);
+  if (q0 <= q1 && offset != 0) {
+    const int cnt = q1 - q0 + 1;
+    int r = (q0 - lo - offset) % len;
+    if (r < 0) r += len;
+    const uint64_t bits = extract_cyclic(in, lo, len, r, cnt);
+    const int sh = q0 - wi * 64;
+    const uint64_t mask = low_mask(cnt) << sh;
+    v = (v & ~mask) | ((bits << sh) & mask);
   }
+  return v;
 }
 
-// random_shift_mutation (ga.cpp:92-104) with the reference's draw order:
-// coin(whole), coin(direction: true = Left), then k, or a, b, k.
-__device__ void random_shift_mutation(const uint64_t* in, uint64_t* out, int m, Stream& rng) {
+__device__ void rotate_range(const uint64_t* in, uint64_t* out, int m, int lo, int len, int offset) {
+  const int wp = (m + 63) >> 6;
+  for (int wi = 0; wi < wp; ++wi) out[wi] = rotate_word(in, lo, len, offset, wi);
+}
+
+// The draws of random_shift_mutation (ga.cpp:92-104) in the reference's order:
+// coin(whole), coin(direction: true = Left), then k, or a, b, k.  Returns the
+// rotated range [lo, lo + len) and its offset.
+struct ShiftDraw {
+  int lo, len, offset;
+};
+
+__device__ __forceinline__ ShiftDraw draw_shift(int m, Stream& rng) {
   const bool whole = rng.coin();
   const bool left = rng.coin();
   if (whole) {
     const int k = 1 + (int)rng.below((uint64_t)(m - 1));
     const int offset = left ? m - k : k;  // ga.cpp:70
-    rotate_range(in, out, m, 0, m, offset % m);
-    return;
+    return ShiftDraw{0, m, offset % m};
   }
   const int a = (int)rng.below((uint64_t)m);
   int b = (int)rng.below((uint64_t)(m - 1));
@@ -108,7 +134,12 @@ __device__ void random_shift_mutation(const uint64_t* in, uint64_t* out, int m, 
   const int len = hi - lo + 1;
   const int k = (int)rng.below((uint64_t)len);
   const int offset = k == 0 ? 0 : (left ? len - k : k);  // ga.cpp:83-85
-  rotate_range(in, out, m, lo, len, offset);
+  return ShiftDraw{lo, len, offset};
+}
+
+__device__ void random_shift_mutation(const uint64_t* in, uint64_t* out, int m, Stream& rng) {
+  const ShiftDraw d = draw_shift(m, rng);
+  rotate_range(in, out, m, d.lo, d.len, d.offset);
 }
 
 // The lowest k set bits of x (all of x when it has at most k).
