@@ -141,6 +141,27 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
     if (payb) PM_CUDA_TRY(c, c->sort_pay.ensure((size_t)bp.grid * 2 * m * payb));
   }
 
+  // counting-sort path: one pass for small cost ranges; two CTAs per SM when
+  // a row's counters + keys fit in half the shared memory (PMB_K1=radix: off)
+  {
+    const char* k1 = getenv("PMB_K1");
+    const int cb = std::max(1, bp.costbits);
+    // (per-row work is O(m + 2^costbits): only rows at least half as long as
+    // the bucket count pay off -- shorter rows keep the radix kernel)
+    if (bp.key_kind == KeyKind::kPacked32 && bp.site_bytes == 2 && cb <= 15 &&
+        (m >= ((size_t)1 << cb) / 2 || (k1 && std::string(k1) == "count")) &&
+        !(k1 && std::string(k1) == "radix")) {
+      const size_t cs = cs_smem(bp.m, cb);
+      if (cs <= c->max_smem) {
+        bp.cs_path = true;
+        bp.cs_bits = cb;
+        const int per_sm = 2 * (cs + 2048) <= 228 * 1024 ? 2 : 1;
+        bp.cs_grid = (int)std::min<size_t>(n, (size_t)c->sms * per_sm);
+        PM_CUDA_TRY(c, c->sort_rows.ensure((n + 1) * sizeof(int)));
+      }
+    }
+  }
+
   c->has_instance = false;
   c->ord.release();
   c->dist.release();
@@ -151,7 +172,7 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   const size_t nP = (n + 15) / 16 * 16;
   PM_CUDA_TRY(c, c->dT.ensure(nP * m * (size_t)bp.dist_bytes));
   PM_CUDA_TRY(c, launch_build_rows(bp, dcosts, c->ord.p, c->dist.p, c->sort_keys.p,
-                                   c->sort_pay.as<uint32_t>(), c->stream));
+                                   c->sort_pay.as<uint32_t>(), c->sort_rows.as<int>(), c->stream));
   PM_CUDA_TRY(c, launch_transpose_costs(dcosts, (int)n, (int)nP, (int)m, bp.dist_bytes, c->dT.p, c->stream));
   c->launches += 2;
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));

@@ -99,7 +99,7 @@ struct pm_ctx {
   DevBuf ord, dist, dT;
 
   // scratch
-  DevBuf costs_in, sort_keys, sort_pay, words, costs_out, T, lists, counts, errw, scal;
+  DevBuf costs_in, sort_keys, sort_pay, sort_rows, words, costs_out, T, lists, counts, errw, scal;
   int open_cap = 0;
   GaBuffers ga;
   cudaStream_t copy_stream = nullptr;  // H2D of pipelined host-buffer calls

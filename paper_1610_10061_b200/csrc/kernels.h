@@ -19,13 +19,20 @@ struct BuildPlan {
   KeyKind key_kind = KeyKind::kPacked64;
   bool smem_path = true;
   int grid = 0;
+  // counting-sort path (k_build_rows_cs): packed u32 keys, u16 sites, costs < 2^15
+  bool cs_path = false;
+  int cs_bits = 0, cs_grid = 0;
 };
+
+size_t cs_smem(int m, int costbits);
 
 size_t sort_smem_header();
 cudaError_t launch_validate_costs(const int64_t* costs, size_t count, unsigned long long* out_max,
                               int* out_neg, int sms, cudaStream_t st);
+// rows: device int[1 + n] (count, then the rows the counting-sort path hands
+// to the radix kernel); used only when bp.cs_path
 cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
-                              void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st);
+                              void* scratch_keys, uint32_t* scratch_pay, int* rows, cudaStream_t st);
 cudaError_t launch_transpose_costs(const int64_t* costs, int n, int nP, int m, int dist_bytes, void* dT,
                                    cudaStream_t st);
 

@@ -259,7 +259,7 @@ template <class KeyT, class OrdT, class DistT, bool kSmem>
 __global__ void __launch_bounds__(kSortThreads, 1)
     k_build_rows_ws(const int64_t* __restrict__ costs, int n, int m, int W, int Wp, int sitebits,
                     int npasses, int dbits, OrdT* __restrict__ ord, DistT* __restrict__ dist,
-                    KeyT* __restrict__ gkeys) {
+                    KeyT* __restrict__ gkeys, const int* __restrict__ rows) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);  // [warp][256]
   uint32_t* tot = cnt + kWsWarps * 256;               // [256]
@@ -274,7 +274,11 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   const int s0 = min(m, warp * slice), s1 = min(m, s0 + slice);
   uint32_t* mycnt = cnt + warp * 256;
 
-  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+  // rows == nullptr: every row; else rows[0] rows listed in rows[1..] (the
+  // rows the counting-sort path handed back)
+  const int nr = rows ? rows[0] : n;
+  for (int ri = blockIdx.x; ri < nr; ri += gridDim.x) {
+    const int r = rows ? rows[1 + ri] : ri;
     const int64_t* crow = costs + (size_t)r * m;
     // keys of the warp's slice, with the first pass's digit histogram (shared
     // atomics: one per key, instead of a ballot ranking pass)
@@ -364,6 +368,129 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   }
 }
 
+// ---- K1 counting-sort path (costs < 2^15, m < 65536) -------------------------
+//
+// One pass instead of ceil(costbits/8) radix passes: a histogram of the row's
+// costs (shared-memory atomics on u16 counters packed in pairs), one block
+// scan, and a scatter through atomic cursors.  The atomics place equal costs in
+// arbitrary order, so each bucket is then put back into ascending site order
+// (the reference's tie-break, ordering.cpp:25-28) by its owning thread with an
+// insertion sort -- buckets are the sites at one exact cost, a handful for
+// metric instances.  A row with a bucket above kCsMaxBucket is handed back
+// (rows list) to the radix kernel, so adversarial ties cost radix time, never
+// quadratic time.  512-thread CTAs, two per SM when the row fits in half the
+// shared memory: one CTA's HBM row load overlaps the other's sort.
+constexpr int kCsThreads = 512;
+constexpr uint32_t kCsMaxBucket = 64;
+
+template <class OrdT, class DistT>
+__global__ void __launch_bounds__(kCsThreads, 2)
+    k_build_rows_cs(const int64_t* __restrict__ costs, int n, int m, int W, int Wp, int sitebits, int costbits,
+                    OrdT* __restrict__ ord, DistT* __restrict__ dist, int* __restrict__ rows) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t wsum[kCsThreads / 32];
+  __shared__ int flag;
+  const int nb = 1 << costbits, nw = nb >> 1;  // buckets; u32 words of two u16 counters
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* out = cnt + nw;  // the sorted row, packed (cost << sitebits | site)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t sitemask = (1u << sitebits) - 1;
+  const int per = (nw + kCsThreads - 1) / kCsThreads;  // counter words owned by a thread in the scan
+  const int w0 = min(nw, tid * per), w1 = min(nw, w0 + per);
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int64_t* crow = costs + (size_t)r * m;
+    for (int x = tid; x < nw; x += kCsThreads) cnt[x] = 0;
+    if (tid == 0) flag = 0;
+    __syncthreads();
+    for (int x = tid; x < m; x += kCsThreads) {
+      const uint32_t c = (uint32_t)crow[x];
+      atomicAdd(&cnt[c >> 1], 1u << ((c & 1) << 4));
+    }
+    __syncthreads();
+    // exclusive scan over the buckets (each thread a contiguous run of words)
+    uint32_t sum = 0;
+    bool big = false;
+    for (int x = w0; x < w1; ++x) {
+      const uint32_t v = cnt[x], lo = v & 0xffffu, hi = v >> 16;
+      sum += lo + hi;
+      big |= lo > kCsMaxBucket || hi > kCsMaxBucket;
+    }
+    if (big) flag = 1;
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t v = lane < kCsThreads / 32 ? wsum[lane] : 0;
+      uint32_t wi = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(kFull, wi, o);
+        if (lane >= o) wi += u;
+      }
+      if (lane < kCsThreads / 32) wsum[lane] = wi - v;
+    }
+    __syncthreads();
+    const bool handback = flag != 0;
+    uint32_t run = wsum[warp] + incl - sum;
+    for (int x = w0; x < w1; ++x) {  // counters become bucket cursors (starts)
+      const uint32_t v = cnt[x], lo = v & 0xffffu, hi = v >> 16;
+      cnt[x] = run | ((run + lo) << 16);
+      run += lo + hi;
+    }
+    __syncthreads();
+    if (handback) {  // CTA-uniform
+      if (tid == 0) rows[1 + atomicAdd(rows, 1)] = r;
+      continue;  // the next row's first barrier orders the reuse of cnt / flag
+    }
+    for (int x = tid; x < m; x += kCsThreads) {  // scatter through atomic cursors
+      const uint32_t c = (uint32_t)crow[x];
+      const uint32_t sh = (c & 1) << 4;
+      const uint32_t old = atomicAdd(&cnt[c >> 1], 1u << sh);
+      out[(old >> sh) & 0xffffu] = (c << sitebits) | (uint32_t)x;
+    }
+    __syncthreads();
+    for (int b = tid; b < nb; b += kCsThreads) {  // bucket b = [end(b-1), end(b)), cursors now at the ends
+      const uint32_t e = (cnt[b >> 1] >> ((b & 1) << 4)) & 0xffffu;
+      const uint32_t s0 = b == 0 ? 0u : (cnt[(b - 1) >> 1] >> (((b - 1) & 1) << 4)) & 0xffffu;
+      for (uint32_t i = s0 + 1; i < e; ++i) {  // insertion sort by site (same cost)
+        const uint32_t key = out[i];
+        uint32_t j = i;
+        while (j > s0 && out[j - 1] > key) {
+          out[j] = out[j - 1];
+          --j;
+        }
+        out[j] = key;
+      }
+    }
+    __syncthreads();
+    OrdT* orow = ord + (size_t)r * Wp;
+    DistT* drow = dist + (size_t)r * Wp;
+    for (int k = tid; k < Wp; k += kCsThreads) {
+      if (k < W) {
+        const uint32_t key = out[k];
+        orow[k] = (OrdT)(key & sitemask);
+        drow[k] = (DistT)(key >> sitebits);
+      } else {
+        orow[k] = (OrdT)m;  // sentinel: T[m] == 0, never open
+        drow[k] = (DistT)0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// rows longer than this would overflow the u16 cursors
+constexpr int kCsMaxM = 65535;
+
+size_t cs_smem(int m, int costbits) {
+  return m > kCsMaxM ? ~(size_t)0 : ((size_t)1 << costbits) / 2 * 4 + (size_t)m * 4;
+}
+
 // ---- site-major narrow cost matrix for the gather-min kernel (K2b) --------
 
 // dT row stride nP = round_up(n, 16): 16-byte vector loads of consecutive
@@ -398,9 +525,23 @@ size_t sort_smem_header() { return ((256 + 256 + 256 * kHistPitch + 4) * 4 + 15)
 
 template <class KeyT, bool kPayload, class OrdT, class DistT>
 static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
-                                 void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st) {
+                                 void* scratch_keys, uint32_t* scratch_pay, int* rows, cudaStream_t st) {
   const size_t per = (size_t)bp.m * (sizeof(KeyT) + (kPayload ? 4 : 0)) * 2;
   const size_t smem = sort_smem_header() + per;
+  if constexpr (!kPayload && sizeof(KeyT) == 4 && sizeof(OrdT) == 2) {
+    if (bp.cs_path) {  // counting sort; rows with large tie buckets go to the radix kernel below
+      const size_t cs = cs_smem(bp.m, bp.cs_bits);
+      auto kern = k_build_rows_cs<OrdT, DistT>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+      if (e != cudaSuccess) return e;
+      e = cudaMemsetAsync(rows, 0, sizeof(int), st);
+      if (e != cudaSuccess) return e;
+      kern<<<bp.cs_grid, kCsThreads, cs, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.cs_bits,
+                                                (OrdT*)ord, (DistT*)dist, rows);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+  }
   if constexpr (!kPayload) {  // packed keys: the warp-slice radix sort
     // npasses = ceil(costbits / 8) passes of balanced digits (<= 8 bits: one
     // ballot per digit bit in the ranking), e.g. 2 x 7 bits for 14-bit costs
@@ -411,13 +552,14 @@ static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       kern<<<bp.grid, kSortThreads, smem, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.npasses, dbits,
-                                                (OrdT*)ord, (DistT*)dist, nullptr);
+                                                (OrdT*)ord, (DistT*)dist, nullptr, bp.cs_path ? rows : nullptr);
     } else {
       auto kern = k_build_rows_ws<KeyT, OrdT, DistT, false>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
       if (e != cudaSuccess) return e;
       kern<<<bp.grid, kSortThreads, hs, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.npasses, dbits,
-                                              (OrdT*)ord, (DistT*)dist, (KeyT*)scratch_keys);
+                                              (OrdT*)ord, (DistT*)dist, (KeyT*)scratch_keys,
+                                              bp.cs_path ? rows : nullptr);
     }
     return cudaGetLastError();
   }
@@ -441,27 +583,27 @@ static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void
 
 template <class OrdT, class DistT>
 static cudaError_t launch_rows_od(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
-                                  void* sk, uint32_t* sp, cudaStream_t st) {
+                                  void* sk, uint32_t* sp, int* rows, cudaStream_t st) {
   switch (bp.key_kind) {
     case KeyKind::kPacked32:
-      return launch_rows_t<uint32_t, false, OrdT, DistT>(bp, costs, ord, dist, sk, sp, st);
+      return launch_rows_t<uint32_t, false, OrdT, DistT>(bp, costs, ord, dist, sk, sp, rows, st);
     case KeyKind::kPacked64:
-      return launch_rows_t<uint64_t, false, OrdT, DistT>(bp, costs, ord, dist, sk, sp, st);
+      return launch_rows_t<uint64_t, false, OrdT, DistT>(bp, costs, ord, dist, sk, sp, rows, st);
     default:
-      return launch_rows_t<uint64_t, true, OrdT, DistT>(bp, costs, ord, dist, sk, sp, st);
+      return launch_rows_t<uint64_t, true, OrdT, DistT>(bp, costs, ord, dist, sk, sp, rows, st);
   }
 }
 
 cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
-                              void* scratch_keys, uint32_t* scratch_pay, cudaStream_t st) {
+                              void* scratch_keys, uint32_t* scratch_pay, int* rows, cudaStream_t st) {
   if (bp.site_bytes == 2) {
-    if (bp.dist_bytes == 2) return launch_rows_od<uint16_t, uint16_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
-    if (bp.dist_bytes == 4) return launch_rows_od<uint16_t, uint32_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
-    return launch_rows_od<uint16_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
+    if (bp.dist_bytes == 2) return launch_rows_od<uint16_t, uint16_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
+    if (bp.dist_bytes == 4) return launch_rows_od<uint16_t, uint32_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
+    return launch_rows_od<uint16_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
   }
-  if (bp.dist_bytes == 2) return launch_rows_od<uint32_t, uint16_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
-  if (bp.dist_bytes == 4) return launch_rows_od<uint32_t, uint32_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
-  return launch_rows_od<uint32_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, st);
+  if (bp.dist_bytes == 2) return launch_rows_od<uint32_t, uint16_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
+  if (bp.dist_bytes == 4) return launch_rows_od<uint32_t, uint32_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
+  return launch_rows_od<uint32_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
 }
 
 cudaError_t launch_transpose_costs(const int64_t* costs, int n, int nP, int m, int dist_bytes, void* dT,

@@ -224,3 +224,23 @@ def test_pipelined_host_call_reports_global_first_bad(ctx, pm, oracle):
     with pytest.raises(pm.ContractError) as ei:
         ctx.evaluate(bad)
     assert ei.value.first_bad == 12001
+
+
+def test_counting_sort_path_and_handback(ctx, oracle):
+    """K1's counting-sort path (costs < 2^15, m >= 2^costbits / 2): ties put back
+    into site order inside each bucket; a row with a bucket above 64 ties is
+    handed to the radix kernel (ordering.cpp:25-28 order either way)."""
+    n, m, p = 24, 9000, 90
+    costs = oracle.random_costs(77, n, m, 10**4).reshape(n, m).copy()
+    costs[3, :] = 4321                       # one bucket of m ties: handed back
+    costs[7, :] = costs[7, :] % 3 + 9000     # three huge buckets
+    costs[11, ::2] = 17                      # half the row tied at one cost
+    costs = costs.reshape(-1)
+    ctx.set_instance(costs, n, m, p)
+    so, inc = oracle.build_ordering(n, m, p, costs)
+    so2, inc2 = ctx.get_tables()
+    assert (so == so2).all() and (inc == inc2).all()
+    pop = oracle.random_population(m, p, 64, seed=5)
+    want = oracle.evaluate(so, inc, m, pop)[1]
+    for kind in KINDS:
+        assert (_eval(ctx, pop, kind) == want).all()
