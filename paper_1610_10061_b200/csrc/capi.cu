@@ -296,7 +296,6 @@ int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcos
                   unsigned long long* errw_override) {
   const DevTables& t = c->t;
   const int wp = (t.m + 63) / 64;
-  PM_CUDA_TRY(c, cudaMemsetAsync(dcosts, 0, count * 8, c->stream));
   unsigned long long* errw = errw_override ? errw_override : c->errw.as<unsigned long long>();
   int kind = c->eval_kind == PM_EVAL_AUTO ? auto_kind(c, count) : c->eval_kind;
   if (mode == 1) kind = PM_EVAL_GATHER;
@@ -308,7 +307,8 @@ int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcos
       return c->fail(PM_DOMAIN, "instance too large for the scan kernel's shared-memory masks; use PM_EVAL_GATHER");
     const size_t groups = (count + 63) / 64;
     PM_CUDA_TRY(c, c->T.ensure(groups * scan_t_stride(t.m) * 8));
-    PM_CUDA_TRY(c, launch_transpose_population(dwords, count, wp, t.m, c->T.as<uint64_t>(), c->stream));
+    PM_CUDA_TRY(c, launch_transpose_population(dwords, count, wp, t.m, c->T.as<uint64_t>(),
+                                               reinterpret_cast<unsigned long long*>(dcosts), c->stream));
     if (c->profiling) {
       ev = c->ev_get();
       cudaEventRecord(ev.first, c->stream);
@@ -319,7 +319,8 @@ int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcos
     PM_CUDA_TRY(c, c->lists.ensure(count * (size_t)c->open_cap * 4));
     PM_CUDA_TRY(c, c->counts.ensure(count * 4));
     PM_CUDA_TRY(c, launch_open_lists(dwords, count, wp, t.m, c->lists.as<uint32_t>(),
-                                     c->counts.as<uint32_t>(), c->open_cap, c->stream));
+                                     c->counts.as<uint32_t>(), c->open_cap,
+                                     reinterpret_cast<unsigned long long*>(dcosts), c->stream));
     if (c->profiling) {
       ev = c->ev_get();
       cudaEventRecord(ev.first, c->stream);

@@ -46,7 +46,8 @@ size_t scan_t_stride(int m) { return ((size_t)m + 1 + 1) / 2 * 2; }
 __global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __restrict__ words,
                                                               size_t count, int wp, int m,
                                                               uint64_t* __restrict__ T,
-                                                              size_t Ts) {
+                                                              size_t Ts,
+                                                              unsigned long long* __restrict__ costs) {
   const int lane = threadIdx.x & 31;
   const int wi = blockIdx.x * 8 + (threadIdx.x >> 5);
   const size_t g = blockIdx.y;
@@ -54,6 +55,9 @@ __global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     for (size_t s = (size_t)m + lane; s < Ts; s += 32) Tg[s] = 0;  // sentinel site m
   }
+  // the scan accumulates into costs: zero the group's 64 (replaces a memset launch)
+  if (blockIdx.x == 0 && threadIdx.x >= 64 && threadIdx.x < 128 && g * 64 + threadIdx.x - 64 < count)
+    costs[g * 64 + threadIdx.x - 64] = 0;
   if (wi >= wp) return;  // warp-uniform
   const size_t c0 = g * 64 + lane, c1 = c0 + 32;
   const uint64_t x = c0 < count ? words[c0 * wp + wi] : 0;
@@ -76,10 +80,10 @@ __global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __
 }
 
 cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int words_per, int m,
-                                        uint64_t* T, cudaStream_t st) {
+                                        uint64_t* T, unsigned long long* costs, cudaStream_t st) {
   const size_t groups = (count + 63) / 64;
   dim3 grid((words_per + 7) / 8, (unsigned)groups);
-  k_transpose_population<<<grid, 256, 0, st>>>(words, count, words_per, m, T, scan_t_stride(m));
+  k_transpose_population<<<grid, 256, 0, st>>>(words, count, words_per, m, T, scan_t_stride(m), costs);
   return cudaGetLastError();
 }
 
@@ -502,10 +506,12 @@ cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* 
 // One warp per chromosome: compact the open sites (< m) into a list.
 __global__ void __launch_bounds__(256) k_open_lists(const uint64_t* __restrict__ words, size_t count,
                                                     int wp, int m, uint32_t* __restrict__ lists,
-                                                    uint32_t* __restrict__ counts, int cap) {
+                                                    uint32_t* __restrict__ counts, int cap,
+                                                    unsigned long long* __restrict__ costs) {
   const size_t c = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (c >= count) return;
   const int lane = threadIdx.x & 31;
+  if (lane == 0) costs[c] = 0;  // the gather accumulates into costs (replaces a memset launch)
   const unsigned lt = lanemask_lt();
   const uint64_t* w = words + c * wp;
   uint32_t* list = lists + c * (size_t)cap;
@@ -676,9 +682,10 @@ static cudaError_t launch_gather_t(const DevTables& t, const uint64_t* words, si
 }
 
 cudaError_t launch_open_lists(const uint64_t* words, size_t count, int words_per, int m,
-                              uint32_t* open_lists, uint32_t* open_counts, int open_cap, cudaStream_t st) {
+                              uint32_t* open_lists, uint32_t* open_counts, int open_cap,
+                              unsigned long long* costs, cudaStream_t st) {
   k_open_lists<<<(unsigned)((count + 7) / 8), 256, 0, st>>>(words, count, words_per, m, open_lists,
-                                                             open_counts, open_cap);
+                                                             open_counts, open_cap, costs);
   return cudaGetLastError();
 }
 
