@@ -90,6 +90,7 @@ cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int
 // ---- K2: bit-sliced scan -------------------------------------------------------
 
 constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
+constexpr int kWideWarps = 24, kWideQueue = 256;  // the many-warp K2 variant (plan_scan)
 
 template <class OrdT, class DistT>
 struct Chunk {
@@ -158,8 +159,8 @@ struct MaskOps {
 // private counters acc[c][lane] (no atomics, no bank conflicts).  The drain
 // loop runs the largest record's bit count, so one lane's burst of hits at a
 // client start no longer stalls the warp.
-template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kDepth>
-__global__ void __launch_bounds__(512, 1)
+template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kDepth, int kW = 0, int kWQ = 128>
+__global__ void __launch_bounds__(kW ? kW * 32 : 512, 1)
     k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
            const uint64_t* __restrict__ T, size_t Ts, size_t count, int groups,
            unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err) {
@@ -167,15 +168,18 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int kG = Ops::kG;
   // row chunks in registers: 3 (two in flight while one is consumed) when the
   // table types are narrow, else 2 to stay within the register budget
-  constexpr int kBufs = sizeof(OrdT) + sizeof(DistT) <= 4 ? 3 : 2;
+  constexpr int kBufs = (kW == 0 && sizeof(OrdT) + sizeof(DistT) <= 4) ? 3 : 2;
+  // queue records per warp: a whole chunk's worth, or (kW: many warps per SM,
+  // less shared memory per warp) kQ with a mid-chunk drain when it could overflow
+  constexpr int kQ = kW ? kWQ : kChunk * 32;
   extern __shared__ __align__(16) unsigned char smem[];
   const int nwarps = blockDim.x >> 5;
   MaskT* Tsm = reinterpret_cast<MaskT*>(smem);
   const size_t tbytes = kTSmem ? (Ts * sizeof(MaskT) + 15) / 16 * 16 : 0;
   AccT* acc = reinterpret_cast<AccT*>(smem + tbytes);                              // [warp][c][lane]
-  MaskT* hbuf = reinterpret_cast<MaskT*>(acc + (size_t)nwarps * kG * 32);           // [warp][j][lane]
-  AccT* dbuf = reinterpret_cast<AccT*>(hbuf + (size_t)nwarps * kChunk * 32);       // [warp][j][lane]
-  int* next_client = reinterpret_cast<int*>(dbuf + (size_t)nwarps * kChunk * 32);
+  MaskT* hbuf = reinterpret_cast<MaskT*>(acc + (size_t)nwarps * kG * 32);           // [warp][kQ]
+  AccT* dbuf = reinterpret_cast<AccT*>(hbuf + (size_t)nwarps * kQ);                // [warp][kQ]
+  int* next_client = reinterpret_cast<int*>(dbuf + (size_t)nwarps * kQ);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = lanemask_lt();
@@ -183,9 +187,9 @@ __global__ void __launch_bounds__(512, 1)
   // the warp's queue of hit columns (at most kChunk * 32 per chunk); a 32-bit
   // mask and a 32-bit cost share one 8-byte record (one STS / LDS)
   constexpr bool kPacked = sizeof(MaskT) == 4 && sizeof(AccT) == 4;
-  MaskT* wqh = hbuf + (size_t)warp * kChunk * 32;
-  AccT* wqd = dbuf + (size_t)warp * kChunk * 32;
-  uint64_t* wq = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kChunk * 32;
+  MaskT* wqh = hbuf + (size_t)warp * kQ;
+  AccT* wqd = dbuf + (size_t)warp * kQ;
+  uint64_t* wq = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kQ;
   (void)wqh;
   (void)wqd;
   (void)wq;
@@ -291,9 +295,39 @@ __global__ void __launch_bounds__(512, 1)
         if constexpr (kTSmem) t[j] = Tsm[cur.site(j)];
         else t[j] = (MaskT)(__ldg(Tg + cur.site(j)) >> half);
       }
+      // drain: lane r applies queue records r, r+32, ... -- the loop runs the
+      // largest record's bit count, not the busiest lane's hit count
+      auto drain = [&](uint32_t qn) {
+        __syncwarp();  // queue writes visible to the draining lanes
+        for (uint32_t base = 0; base < qn; base += 32) {
+          MaskT h = 0;
+          AccT dv = 0;
+          if (base + lane < qn) {
+            if constexpr (kPacked) {
+              const uint64_t x = wq[base + lane];
+              h = (MaskT)x;
+              dv = (AccT)(x >> 32);
+            } else {
+              h = wqh[base + lane];
+              dv = wqd[base + lane];
+            }
+          }
+          while (h) {
+            const int c = Ops::pop_high(h);
+            myacc[c * 32] += dv;
+          }
+        }
+        __syncwarp();  // the queue is rewritten next
+      };
       uint32_t qn = 0;  // warp-uniform queue length
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
+        if constexpr (kQ < kChunk * 32) {
+          if (qn > (uint32_t)(kQ - 32)) {  // warp-uniform: the next column could overflow
+            drain(qn);
+            qn = 0;
+          }
+        }
         const MaskT h = alive & t[j];
         alive &= ~t[j];
         const unsigned hb = __ballot_sync(kFull, h != 0);
@@ -311,28 +345,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         qn += __popc(hb);
       }
-      __syncwarp();  // queue writes visible to the draining lanes
-      // drain: lane r applies queue records r, r+32, ... -- the loop runs the
-      // largest record's bit count, not the busiest lane's hit count
-      for (uint32_t base = 0; base < qn; base += 32) {
-        MaskT h = 0;
-        AccT dv = 0;
-        if (base + lane < qn) {
-          if constexpr (kPacked) {
-            const uint64_t x = wq[base + lane];
-            h = (MaskT)x;
-            dv = (AccT)(x >> 32);
-          } else {
-            h = wqh[base + lane];
-            dv = wqd[base + lane];
-          }
-        }
-        while (h) {
-          const int c = Ops::pop_high(h);
-          myacc[c * 32] += dv;
-        }
-      }
-      __syncwarp();  // the next step rewrites the queue
+      drain(qn);
       if (i >= 0) {
         k += kChunk;
         if (alive == 0 || k >= Wp) {
@@ -369,10 +382,10 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
-static size_t scan_smem(int m, int warps, bool acc32, bool tsmem, int G) {
+static size_t scan_smem(int m, int warps, bool acc32, bool tsmem, int G, int qrec = kChunk * 32) {
   const size_t ab = acc32 ? 4 : 8, mb = G / 8;
   const size_t tb = tsmem ? (scan_t_stride(m) * mb + 15) / 16 * 16 : 0;
-  return tb + (size_t)warps * 32 * (G * ab + kChunk * (mb + ab)) + 16;
+  return tb + (size_t)warps * (32 * G * ab + (size_t)qrec * (mb + ab)) + 16;
 }
 
 template <class OrdT, class DistT, class AccT, bool kDepth>
@@ -392,7 +405,10 @@ static const void* scan_fn_acc(int G, bool tsmem) {
                  : scan_fn_depth<OrdT, DistT, AccT, false>(G, tsmem);
 }
 
-static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool ts) {
+static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool ts, int wide = 0) {
+  if (wide && t.site_bytes == 2 && t.dist_bytes == 2 && acc32 && G == 32 && ts && !g_depth)
+    return reinterpret_cast<const void*>(
+        k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue>);
   if (t.site_bytes == 2) {
     if (t.dist_bytes == 2) return acc32 ? scan_fn_acc<uint16_t, uint16_t, uint32_t>(G, ts) : scan_fn_acc<uint16_t, uint16_t, uint64_t>(G, ts);
     if (t.dist_bytes == 4) return acc32 ? scan_fn_acc<uint16_t, uint32_t, uint32_t>(G, ts) : scan_fn_acc<uint16_t, uint32_t, uint64_t>(G, ts);
@@ -463,6 +479,22 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
         sp.acc32 = acc32;
         sp.smem = smem;
         sp.ctas = ctas;
+        // long segments, narrow tables: the many-warp variant (24 warps, 80
+        // registers, two row chunks in flight, a 256-record queue drained
+        // mid-chunk when it could overflow) -- measured 7 % faster at syn20k
+        // than 16 warps with three chunks (tools/wide_sweep.sh: 20-32 warps,
+        // 64-256 records); PMB_SCAN_WIDE=0 turns it off
+        const char* ew = getenv("PMB_SCAN_WIDE");
+        if (!fG && !split && !(ew && ew[0] == '0') && sp.G == 32 && sp.tsmem && sp.acc32 && !depth_mode &&
+            t.site_bytes == 2 && t.dist_bytes == 2) {
+          const size_t sm2 = scan_smem(t.m, kWideWarps, true, true, 32, kWideQueue);
+          if (sm2 <= max_smem) {
+            sp.wide = 1;
+            sp.warps = kWideWarps;
+            sp.ctas = sms;
+            sp.smem = sm2;
+          }
+        }
         return sp;
       }
     }
@@ -475,7 +507,7 @@ cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* 
                         unsigned long long* costs_acc, unsigned long long* err_first_bad,
                         int depth_mode, cudaStream_t st) {
   g_depth = depth_mode != 0;
-  const void* fn = scan_kernel_ptr(t, sp.acc32, sp.G, sp.tsmem);
+  const void* fn = scan_kernel_ptr(t, sp.acc32, sp.G, sp.tsmem, sp.wide);
   // raise the kernel's dynamic shared-memory cap only when it grows (the call
   // costs host time on every launch otherwise; the GA launches K2 ~10x per generation)
   static thread_local std::vector<std::pair<const void*, size_t>> raised;
