@@ -159,8 +159,11 @@ struct MaskOps {
 // private counters acc[c][lane] (no atomics, no bank conflicts).  The drain
 // loop runs the largest record's bit count, so one lane's burst of hits at a
 // client start no longer stalls the warp.
-template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kDepth, int kW = 0, int kWQ = 128>
-__global__ void __launch_bounds__(kW ? kW * 32 : 512, 1)
+// kW > 0: the many-warp variant -- kW warps per SM in CTAs of kCtaW warps
+// (registers capped at 64K / (32 kW)), a kWQ-record queue, two row chunks.
+template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kDepth, int kW = 0, int kWQ = 128,
+          int kCtaW = kW>
+__global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCtaW : 1) : 1)
     k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
            const uint64_t* __restrict__ T, size_t Ts, size_t count, int groups,
            unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err) {
@@ -406,9 +409,12 @@ static const void* scan_fn_acc(int G, bool tsmem) {
 }
 
 static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool ts, int wide = 0) {
-  if (wide && t.site_bytes == 2 && t.dist_bytes == 2 && acc32 && G == 32 && ts && !g_depth)
-    return reinterpret_cast<const void*>(
-        k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue>);
+  if (wide && t.site_bytes == 2 && t.dist_bytes == 2 && acc32 && G == 32 && ts && !g_depth) {
+    // wide = warps per CTA of the variant (kWideWarps: one CTA per SM)
+    if (wide == 2) return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue, 2>);
+    if (wide == 4) return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue, 4>);
+    return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue>);
+  }
   if (t.site_bytes == 2) {
     if (t.dist_bytes == 2) return acc32 ? scan_fn_acc<uint16_t, uint16_t, uint32_t>(G, ts) : scan_fn_acc<uint16_t, uint16_t, uint64_t>(G, ts);
     if (t.dist_bytes == 4) return acc32 ? scan_fn_acc<uint16_t, uint32_t, uint32_t>(G, ts) : scan_fn_acc<uint16_t, uint32_t, uint64_t>(G, ts);
@@ -489,10 +495,28 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
             t.site_bytes == 2 && t.dist_bytes == 2) {
           const size_t sm2 = scan_smem(t.m, kWideWarps, true, true, 32, kWideQueue);
           if (sm2 <= max_smem) {
-            sp.wide = 1;
+            sp.wide = kWideWarps;
             sp.warps = kWideWarps;
             sp.ctas = sms;
             sp.smem = sm2;
+          }
+        }
+        // split shapes (short segments): the same variant as 12 x 2-warp (or
+        // 6 x 4-warp) CTAs per SM when the CTAs' masks fit -- small m, e.g. the
+        // paper's GA shape: pmed40 0.079 -> 0.074 ms (8-warp CTAs lose to the
+        // 16-warp split shapes; tools/splitw_sweep.sh)
+        if (!fG && split && !(ew && ew[0] == '0') && sp.G == 32 && sp.tsmem && sp.acc32 && !depth_mode &&
+            t.site_bytes == 2 && t.dist_bytes == 2) {
+          for (int cw : {2, 4}) {
+            const size_t sm2 = scan_smem(t.m, cw, true, true, 32, kWideQueue);
+            const int cps = kWideWarps / cw;
+            if (sm2 <= max_smem && (size_t)cps * (sm2 + 1024) <= l1_total) {
+              sp.wide = cw;
+              sp.warps = cw;
+              sp.ctas = sms * cps;
+              sp.smem = sm2;
+              break;
+            }
           }
         }
         return sp;
