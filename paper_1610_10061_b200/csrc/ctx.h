@@ -78,6 +78,7 @@ struct HostBuf {
 // record {cost, thread, words[wp]} per block (k_block_min).
 struct GaBuffers {
   DevBuf pop, next, cost, before, child, ccost, ok, brec, evals, tmp, table, ranks, rflags, rstate;
+  DevBuf lfact;  // ln x! for x <= m + 1 (double): the unranking's search guide
   HostBuf hrec, hmig;
 };
 }  // namespace pmb

@@ -393,6 +393,143 @@ __global__ void __launch_bounds__(256) k_unrank(const uint64_t* __restrict__ ran
   if (active && gl == 0 && word) w[word_idx] = word;
 }
 
+// Reference-exact unranking, one thread per chromosome, guided by logarithms:
+// the next taken candidate is the smallest j with C(a-j, k+1) < X, and
+// ln C(x, y) = ln x! - ln y! - ln (x-y)! is monotone in j, so a binary search
+// over a table of ln x! (doubles) lands on j or next to it; two exact
+// multi-limb comparisons against the Pascal table (C(a-j, k+1) < X and, for
+// j > 0, C(a-j+1, k+1) >= X) confirm it or step it by one.  The doubles only
+// guide; every decision is exact, so the subsets are the reference's bit for
+// bit.  ~p exact probes of one entry each instead of ~p * E[gap]/S probes of S
+// entries: far less work than the lane-group probe (k_unrank).
+template <int kL>
+__device__ __forceinline__ void load_entry(const uint64_t* __restrict__ table, int m, int L, int y, int x, int lim,
+                                           uint64_t (&cv)[kL]) {
+  // C(x, y) as kL limbs (the top ones beyond this step's lim are zero); 0 for x < y
+  const uint64_t* cp = table + (size_t)y * L * m + (x < y ? 0 : x);
+#pragma unroll
+  for (int i = 0; i < kL; ++i) cv[i] = (i < lim && x >= y) ? __ldg(cp + (size_t)i * m) : 0;
+}
+
+template <int kL>
+__device__ __forceinline__ int cmp_limbs(const uint64_t (&cv)[kL], const uint64_t (&X)[kL]) {
+  int cmp = 0;  // sign of cv - X
+#pragma unroll
+  for (int i = kL - 1; i >= 0; --i)
+    if (cmp == 0) cmp = cv[i] < X[i] ? -1 : (cv[i] > X[i] ? 1 : 0);
+  return cmp;
+}
+
+// Reference-exact unranking, one thread per chromosome, guided by logarithms:
+// the next taken candidate is the smallest j with C(a-j, k+1) < X, and
+// ln C(x, y) = ln x! - ln y! - ln (x-y)! is monotone in j, so a binary search
+// over a table of ln x! (doubles, in shared memory) lands on j or next to it;
+// exact multi-limb comparisons against the Pascal table (C(a-j, k+1) < X and,
+// for j > 0, C(a-j+1, k+1) >= X; both entries loaded together) confirm it or
+// step it by one.  The doubles only guide; every decision is exact, so the
+// subsets are the reference's bit for bit.  One L2 round trip per taken
+// element instead of ~E[gap]/S probes of S entries (k_unrank).
+template <int kL>
+__global__ void __launch_bounds__(128) k_unrank_log(const uint64_t* __restrict__ ranks,
+                                                    const uint64_t* __restrict__ table,
+                                                    const double* __restrict__ lf_g, int m, int p, int L, int wp,
+                                                    int count, uint64_t* __restrict__ out) {
+  extern __shared__ double lf_s[];  // m + 2 entries when they fit (see launch), else unused
+  const bool in_smem = lf_s != nullptr && (size_t)(m + 2) * 8 <= 48 * 1024;
+  if (in_smem)
+    for (int x = threadIdx.x; x < m + 2; x += blockDim.x) lf_s[x] = lf_g[x];
+  __syncthreads();
+  const double* lf = in_smem ? lf_s : lf_g;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= count) return;
+  const uint64_t* bound = table + (size_t)(p + 1) * L * m;
+  const uint64_t* lims = bound + L;  // limbs of C(m, k + 1), k < p
+  uint64_t X[kL];                    // X = C(m, p) - r
+  {
+    uint64_t borrow = 0;
+#pragma unroll
+    for (int i = 0; i < kL; ++i) {
+      if (i < L) {
+        const uint64_t b = __ldg(bound + i), r = __ldg(ranks + (size_t)idx * L + i);
+        X[i] = b - r - borrow;
+        borrow = (b < r) || (b - r < borrow);
+      } else {
+        X[i] = 0;
+      }
+    }
+  }
+  uint64_t* w = out + (size_t)idx * wp;
+  for (int i = 0; i < wp; ++i) w[i] = 0;
+  int a = m - 1, k = p - 1;
+  int word_idx = 0;
+  uint64_t word = 0;
+  uint64_t cv[kL], cw[kL];
+  while (k >= 0) {
+    const int lim = (int)__ldg(lims + k);
+    // ln X from its top two limbs
+    double lX = 0.0;
+    {
+      bool found = false;
+#pragma unroll
+      for (int i = kL - 1; i >= 0; --i) {
+        if (!found && X[i] != 0) {
+          found = true;
+          const double lo = i > 0 ? (double)X[i - 1] * 5.421010862427522e-20 : 0.0;  // 2^-64
+          lX = log((double)X[i] + lo) + (double)i * 44.3614195558365;              // 64 ln 2
+        }
+      }
+    }
+    // smallest j in [0, a-k] with ln C(a-j, k+1) < ln X (C(k, k+1) = 0 at j = a-k)
+    const double lk = lf[k + 1];
+    int lo = 0, hi = a - k;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1, x = a - mid;
+      const double lc = lf[x] - lk - lf[x - k - 1];
+      if (lc < lX) hi = mid;
+      else lo = mid + 1;
+    }
+    int j = lo;
+    // exact confirmation (both entries in flight together), stepping by one
+    // when the estimate is off
+    load_entry<kL>(table, m, L, k + 1, a - j, lim, cv);
+    if (j > 0) load_entry<kL>(table, m, L, k + 1, a - j + 1, lim, cw);
+    while (true) {
+      if (cmp_limbs<kL>(cv, X) >= 0) {  // C(a-j, k+1) >= X: the taken one is further
+        ++j;
+#pragma unroll
+        for (int i = 0; i < kL; ++i) cw[i] = cv[i];
+        load_entry<kL>(table, m, L, k + 1, a - j, lim, cv);
+        continue;
+      }
+      if (j > 0 && cmp_limbs<kL>(cw, X) < 0) {  // C(a-j+1, k+1) < X too: it is earlier
+        --j;
+#pragma unroll
+        for (int i = 0; i < kL; ++i) cv[i] = cw[i];
+        if (j > 0) load_entry<kL>(table, m, L, k + 1, a - j + 1, lim, cw);
+        continue;
+      }
+      break;
+    }
+    uint64_t borrow = 0;
+#pragma unroll
+    for (int i = 0; i < kL; ++i) {
+      const uint64_t d = X[i] - cv[i] - borrow;
+      borrow = (X[i] < cv[i]) || (X[i] - cv[i] < borrow);
+      X[i] = d;
+    }
+    const int cand = m - 1 - a + j;
+    if ((cand >> 6) != word_idx) {
+      if (word) w[word_idx] = word;
+      word_idx = cand >> 6;
+      word = 0;
+    }
+    word |= 1ull << (cand & 63);
+    a -= j + 1;
+    --k;
+  }
+  if (word) w[word_idx] = word;
+}
+
 // Lanes per chromosome for k_unrank: the width S minimising the expected warp
 // work per draw, (S/32) * E[probes per gap] = (S/32) / (1 - (1 - p/m)^S)
 // (PMB_UNRANK_S overrides, for tuning).
@@ -751,6 +888,10 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
   if (ref_draw && hd.L) {  // the Pascal table for device unranking, once per run
     const std::vector<uint64_t> tab = binomial_table(s.m, s.p, hd.L);
     PM_CUDA_TRY(c, B.table.ensure(tab.size() * 8));
+    std::vector<double> lfact((size_t)s.m + 2);  // ln x!, the search guide of k_unrank_log
+    for (size_t x = 0; x < lfact.size(); ++x) lfact[x] = std::lgamma((double)x + 1.0);
+    PM_CUDA_TRY(c, B.lfact.ensure(lfact.size() * 8));
+    PM_CUDA_TRY(c, cudaMemcpyAsync(B.lfact.p, lfact.data(), lfact.size() * 8, cudaMemcpyHostToDevice, c->stream));
     PM_CUDA_TRY(c, B.ranks.ensure(count * hd.L * 8));
     // stream-ordered upload: a plain cudaMemcpy runs on the legacy stream, which
     // does not order against the context's non-blocking streams (the first
@@ -784,7 +925,16 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 2;
       const int S = pick_unrank_group(s.m, s.p);
-      if (L <= 8) launch_unrank<8>(S, B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>(), ds);
+      const char* ue = getenv("PMB_UNRANK");
+      if (!(ue && std::string(ue) == "probe")) {  // log-guided search (default)
+        const unsigned gl = cdiv(count, 128);
+        const double* lf = B.lfact.as<double>();
+        uint64_t* o = dst.as<uint64_t>();
+        const size_t lsm = (size_t)(s.m + 2) * 8 <= 48 * 1024 ? (size_t)(s.m + 2) * 8 : 0;
+        if (L <= 8) k_unrank_log<8><<<gl, 128, lsm, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), lf, s.m, s.p, L, (int)wp, (int)count, o);
+        else if (L <= 16) k_unrank_log<16><<<gl, 128, lsm, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), lf, s.m, s.p, L, (int)wp, (int)count, o);
+        else k_unrank_log<32><<<gl, 128, lsm, ds>>>(B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), lf, s.m, s.p, L, (int)wp, (int)count, o);
+      } else if (L <= 8) launch_unrank<8>(S, B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>(), ds);
       else if (L <= 16) launch_unrank<16>(S, B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>(), ds);
       else launch_unrank<32>(S, B.ranks.as<uint64_t>(), B.table.as<uint64_t>(), s.m, s.p, L, (int)wp, (int)count, dst.as<uint64_t>(), ds);
       PM_CUDA_TRY(c, cudaGetLastError());
