@@ -163,25 +163,41 @@ __device__ bool crossover(const uint64_t* a, const uint64_t* b, uint64_t* child,
   for (int wi = 0; wi < wp; ++wi) child[wi] = a[wi];
   int oq = exchanges / 2, cq = exchanges / 2;
   bool done = oq == 0 && cq == 0;
-  for (int step = 0; step <= wp; ++step) {
-    if (done) break;
-    const bool first = step < wp - sw;  // [start, m) first, then [0, start)
-    const int wi = first ? sw + step : step - (wp - sw);
-    uint64_t range = ~0ull;
-    if (first) {
-      if (wi == sw) range &= ~0ull << (start & 63);
-      if (wi == wp - 1) range &= low_mask(((m - 1) & 63) + 1);
-    } else if (wi == sw) {
-      range &= low_mask(start & 63);
+  // steps in groups of 4 whose parent words are loaded up front (4 loads in
+  // flight instead of one dependent round trip per step); still one flat loop
+  // per group with no early exit
+  for (int s0 = 0; s0 <= wp && !done; s0 += 4) {
+    uint64_t aw[4], bw[4];
+    int wis[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int step = s0 + u;
+      const bool first = step < wp - sw;  // [start, m) first, then [0, start)
+      wis[u] = first ? sw + step : step - (wp - sw);
+      aw[u] = step <= wp ? a[wis[u]] : 0;
+      bw[u] = step <= wp ? b[wis[u]] : 0;
     }
-    const uint64_t aw = a[wi];
-    const uint64_t diff = (aw ^ b[wi]) & range;
-    const uint64_t take_o = lowest_bits(diff & ~aw, oq);
-    const uint64_t take_c = lowest_bits(diff & aw, cq);
-    oq -= __popcll(take_o);
-    cq -= __popcll(take_c);
-    child[wi] = (child[wi] | take_o) & ~take_c;
-    done = oq == 0 && cq == 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int step = s0 + u;
+      if (step > wp || done) continue;
+      const bool first = step < wp - sw;
+      const int wi = wis[u];
+      uint64_t range = ~0ull;
+      if (first) {
+        if (wi == sw) range &= ~0ull << (start & 63);
+        if (wi == wp - 1) range &= low_mask(((m - 1) & 63) + 1);
+      } else if (wi == sw) {
+        range &= low_mask(start & 63);
+      }
+      const uint64_t diff = (aw[u] ^ bw[u]) & range;
+      const uint64_t take_o = lowest_bits(diff & ~aw[u], oq);
+      const uint64_t take_c = lowest_bits(diff & aw[u], cq);
+      oq -= __popcll(take_o);
+      cq -= __popcll(take_c);
+      child[wi] = (child[wi] | take_o) & ~take_c;
+      done = oq == 0 && cq == 0;
+    }
   }
   return done;
 }
