@@ -244,3 +244,19 @@ def test_counting_sort_path_and_handback(ctx, oracle):
     want = oracle.evaluate(so, inc, m, pop)[1]
     for kind in KINDS:
         assert (_eval(ctx, pop, kind) == want).all()
+
+
+@pytest.mark.parametrize("npts,p,count", [(20000, 200, 2048), (900, 90, 15360)])
+def test_scan_shapes_agree(ctx, oracle, npts, p, count, monkeypatch):
+    """The planner's 24-warp K2 variant (one 768-thread CTA per SM for long
+    segments, 12 x 2-warp CTAs for short ones) and the 16-warp shapes it
+    replaces (PMB_SCAN_WIDE=0) give identical costs."""
+    costs = oracle.synth_euclid(npts)
+    ctx.set_instance(costs, npts, npts, p)
+    pop = oracle.random_population(npts, p, count, seed=3)
+    wide = _eval(ctx, pop, 1)
+    monkeypatch.setenv("PMB_SCAN_WIDE", "0")
+    narrow = _eval(ctx, pop, 1)
+    assert (wide == narrow).all()
+    for r in range(0, count, count // 4):
+        assert oracle.min_cost_sum(npts, npts, costs, pop[r]) == (0, wide[r])
