@@ -9,7 +9,9 @@ LIB       := $(PKG)/libpmedian_b200.so
 
 CLI       := $(PKG)/pmedian_bench
 
-all: $(LIB) $(CLI) oracle
+REFTESTS  := tests/cpp/_ref/ref_tests
+
+all: $(LIB) $(CLI) oracle reftests
 
 build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/pmedian_b200.h
 	@mkdir -p build
@@ -25,8 +27,21 @@ $(CLI): $(PKG)/cli/pmedian_bench.cpp $(LIB) $(PKG)/csrc/combinatorics.h
 oracle:
 	$(MAKE) -s -C oracle
 
+# TEST INFRASTRUCTURE: the reference's own unit tests (test_chromosome,
+# test_instance, test_formulation) compiled unchanged against the compat
+# headers (include/compat/pmedian/ -> the device path) with a doctest stand-in.
+# Built where /root/reference exists; the binary travels with the snapshot.
+REF_TESTS_DIR ?= /root/reference/proj/tests
+reftests: $(LIB)
+	@if [ -d "$(REF_TESTS_DIR)" ]; then \
+	  mkdir -p tests/cpp/_ref && \
+	  g++ -std=c++20 -O1 -I include/compat -I include -I tests/cpp/doctest_shim tests/cpp/ref_tests_main.cpp \
+	    $(REF_TESTS_DIR)/test_chromosome.cpp $(REF_TESTS_DIR)/test_instance.cpp $(REF_TESTS_DIR)/test_formulation.cpp \
+	    -L $(PKG) -lpmedian_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)' -o $(REFTESTS).tmp && mv $(REFTESTS).tmp $(REFTESTS); \
+	else echo "reftests: $(REF_TESTS_DIR) absent, keeping prebuilt $(REFTESTS) (if any)"; fi
+
 clean:
 	rm -rf build $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle reftests clean

@@ -1,0 +1,141 @@
+// pmedian/instance.hpp, B200 compat layer: the reference's Instance API
+// (proj/include/pmedian/instance.hpp:15-53) with the same signatures, errors and
+// texts, backed by the device path.  Constructing an Instance uploads the cost
+// matrix once and builds the ordering tables on the GPU (pm_set_instance: the
+// validation of instance.cpp:10-30, then K1); min_cost_sum, direct_cost and
+// exact_optimum_small evaluate on the device (K2b).  Copies share the one
+// resident device instance, which is immutable after construction; calls into
+// it are serialised.  Link with libpmedian_b200.so.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cstdlib>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <span>
+#include <vector>
+
+#include "pmedian/chromosome.hpp"
+#include "pmedian/errors.hpp"
+#include "pmedian_b200.hpp"
+
+namespace pmedian {
+
+namespace detail {
+// One device context holding the instance's resident tables.
+struct Device {
+  std::mutex mu;
+  b200::Tables tables;
+  explicit Device(int device) : tables(device) {}
+};
+inline int default_device() {
+  const char* d = std::getenv("PMEDIAN_B200_DEVICE");
+  return d ? std::atoi(d) : 0;
+}
+}  // namespace detail
+
+class Instance {
+ public:
+  Instance(std::size_t clients, std::size_t sites, std::size_t open_count, std::vector<std::int64_t> costs)
+      : clients_(clients), sites_(sites), open_count_(open_count), costs_(std::move(costs)) {
+    // argument checks in the reference's order (instance.cpp:13-18); the cost
+    // checks (non-negative, no int64 overflow of n * max) run on the device
+    if (clients_ == 0) throw StructuralError("instance needs at least one client");
+    if (sites_ == 0) throw StructuralError("instance needs at least one site");
+    if (open_count_ < 1) throw DomainError("p must be >= 1");
+    if (open_count_ >= sites_) throw DomainError("p must be < m");
+    if (costs_.size() != clients_ * sites_) throw StructuralError("cost matrix must be exactly n rows by m columns");
+    device_ = std::make_shared<detail::Device>(detail::default_device());
+    device_->tables.build(costs_, clients_, sites_, open_count_);
+  }
+
+  std::size_t clients() const { return clients_; }
+  std::size_t sites() const { return sites_; }
+  std::size_t open_count() const { return open_count_; }
+  std::int64_t cost(std::size_t i, std::size_t j) const { return costs_[i * sites_ + j]; }
+  std::span<const std::int64_t> row(std::size_t i) const { return {costs_.data() + i * sites_, sites_}; }
+  const std::vector<std::int64_t>& costs() const { return costs_; }
+
+  // the resident device instance (build_ordering, fitness, evolve_block, run_ga use it)
+  const std::shared_ptr<detail::Device>& device() const { return device_; }
+
+ private:
+  std::size_t clients_, sites_, open_count_;
+  std::vector<std::int64_t> costs_;
+  std::shared_ptr<detail::Device> device_;
+};
+
+// Sum over clients of the cheapest open site (instance.cpp:32-48), on the device.
+inline std::int64_t min_cost_sum(const Instance& inst, const Chromosome& c) {
+  if (c.size() != inst.sites()) throw StructuralError("chromosome length must equal the site count");
+  std::lock_guard<std::mutex> lock(inst.device()->mu);
+  return inst.device()->tables.min_cost_sum(c.words(), 1)[0];
+}
+
+// min_cost_sum with the exactly-p contract (instance.cpp:50-58).
+inline std::int64_t direct_cost(const Instance& inst, const Chromosome& c) {
+  if (c.size() != inst.sites()) throw StructuralError("chromosome length must equal the site count");
+  if (c.popcount() != inst.open_count()) throw ContractError("chromosome must open exactly p sites");
+  return min_cost_sum(inst, c);
+}
+
+struct ExactOptimum {
+  Chromosome best;
+  std::int64_t cost = 0;
+};
+
+// Exhaustive search over all p-subsets (instance.cpp:76-110): subsets are
+// enumerated on the host in lexicographic order and evaluated on the device in
+// batches; the first strict minimum wins, as in the reference.
+inline ExactOptimum exact_optimum_small(const Instance& inst, std::uint64_t subset_budget = 10'000'000) {
+  const std::size_t m = inst.sites(), p = inst.open_count();
+  {  // C(m, p), saturated above the budget
+    unsigned __int128 r = 1;
+    const std::uint64_t q = p < m - p ? p : m - p;
+    for (std::uint64_t i = 1; i <= q; ++i) {
+      r = r * (m - q + i) / i;
+      if (r > subset_budget) throw BudgetError("instance too large for the exhaustive oracle");
+    }
+  }
+  const std::size_t wp = (m + 63) / 64, batch = 1 << 16;
+  std::vector<std::size_t> pick(p);
+  for (std::size_t j = 0; j < p; ++j) pick[j] = j;
+  std::vector<std::uint64_t> words;
+  std::vector<std::vector<std::size_t>> picks;
+  std::int64_t best_cost = std::numeric_limits<std::int64_t>::max();
+  std::vector<std::size_t> best_pick;
+  bool more = true;
+  while (more) {
+    words.assign(batch * wp, 0);
+    picks.clear();
+    std::size_t k = 0;
+    for (; k < batch && more; ++k) {
+      for (const std::size_t j : pick) words[k * wp + (j >> 6)] |= std::uint64_t{1} << (j & 63);
+      picks.push_back(pick);
+      std::size_t j = p;  // next subset in lexicographic order
+      while (j > 0 && pick[j - 1] == m - p + (j - 1)) --j;
+      if (j == 0) {
+        more = false;
+      } else {
+        ++pick[j - 1];
+        for (std::size_t t = j; t < p; ++t) pick[t] = pick[t - 1] + 1;
+      }
+    }
+    words.resize(k * wp);
+    std::vector<std::int64_t> costs;
+    {
+      std::lock_guard<std::mutex> lock(inst.device()->mu);
+      costs = inst.device()->tables.min_cost_sum(words, k);
+    }
+    for (std::size_t i = 0; i < k; ++i)
+      if (costs[i] < best_cost) {
+        best_cost = costs[i];
+        best_pick = picks[i];
+      }
+  }
+  return {Chromosome::from_open(m, best_pick), best_cost};
+}
+
+}  // namespace pmedian
