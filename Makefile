@@ -28,7 +28,7 @@ oracle:
 	$(MAKE) -s -C oracle
 
 # TEST INFRASTRUCTURE: the reference's own unit tests (test_chromosome,
-# test_instance, test_formulation) compiled unchanged against the compat
+# test_instance, test_formulation, test_ga) compiled unchanged against the compat
 # headers (include/compat/pmedian/ -> the device path) with a doctest stand-in.
 # Built where /root/reference exists; the binary travels with the snapshot.
 REF_TESTS_DIR ?= /root/reference/proj/tests
@@ -37,6 +37,7 @@ reftests: $(LIB)
 	  mkdir -p tests/cpp/_ref && \
 	  g++ -std=c++20 -O1 -I include/compat -I include -I tests/cpp/doctest_shim tests/cpp/ref_tests_main.cpp \
 	    $(REF_TESTS_DIR)/test_chromosome.cpp $(REF_TESTS_DIR)/test_instance.cpp $(REF_TESTS_DIR)/test_formulation.cpp \
+	    $(REF_TESTS_DIR)/test_ga.cpp \
 	    -L $(PKG) -lpmedian_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)' -o $(REFTESTS).tmp && mv $(REFTESTS).tmp $(REFTESTS); \
 	else echo "reftests: $(REF_TESTS_DIR) absent, keeping prebuilt $(REFTESTS) (if any)"; fi
 

@@ -2,9 +2,11 @@
 // BlockResult, evolve_block and run_ga with the reference's signatures
 // (proj/include/pmedian/ga.hpp:14-109), run by the device GA (K3/K2):
 // bit-identical blocks and RunResults (tests/test_gpu_ga.py, tests/cpp).
-// The reference's operator-level helpers (crossover, circular_shift,
-// block_shift, random_shift_mutation, crossover_couple, block_min_reduce) run
-// inside the device kernels and are not exported here.
+// The operator-level helpers (crossover, circular_shift, block_shift,
+// random_shift_mutation, crossover_couple, block_min_reduce) are provided as
+// host functions with the reference's semantics for callers that use them
+// directly; the GA itself never calls them -- evolve_block and run_ga run the
+// device kernels (csrc/ga_ops.cuh restates the same operators word-wise).
 // Deviation: evolve_block requires every chromosome of the block to open
 // exactly p sites (the GA invariant) and says so up front (DomainError).
 #pragma once
@@ -71,6 +73,90 @@ struct BlockResult {
   std::int64_t cost = 0;
   std::size_t thread = 0;
 };
+
+// ---- operator-level helpers (host; ga.hpp:59-91 of the reference) ----------
+
+// Balanced gene exchange (ga.cpp:35-63): scanning cyclically from start_index,
+// differing positions adopt b's gene while each direction's quota
+// (exchange_count / 2) lasts; nothing when the quotas cannot both be met.
+inline std::optional<Chromosome> crossover(const Chromosome& a, const Chromosome& b, std::size_t start_index,
+                                           std::size_t exchange_count) {
+  if (a.size() != b.size()) throw StructuralError("parents must have equal length");
+  const std::size_t m = a.size(), p = a.popcount();
+  if (start_index >= m) throw DomainError("crossover start index out of range");
+  if (exchange_count < 2 || exchange_count % 2 != 0 || exchange_count / 2 > p / 2)
+    throw DomainError("exchange count must be even, between 2 and 2*(popcount/2)");
+  Chromosome child = a;
+  std::size_t to_open = exchange_count / 2, to_close = exchange_count / 2;
+  for (std::size_t s = 0; s < m && (to_open || to_close); ++s) {
+    const std::size_t j = (start_index + s) % m;
+    const bool ia = a.test(j);
+    if (ia == b.test(j)) continue;
+    if (!ia && to_open) {
+      child.set(j, true);
+      --to_open;
+    } else if (ia && to_close) {
+      child.set(j, false);
+      --to_close;
+    }
+  }
+  if (to_open || to_close) return std::nullopt;
+  return child;
+}
+
+// Whole-vector rotation by k (ga.cpp:65-75): Right moves bit j to j + k.
+inline Chromosome circular_shift(const Chromosome& c, std::size_t k, ShiftDirection direction) {
+  const std::size_t m = c.size();
+  if (k >= m) throw DomainError("shift distance must be < the vector length");
+  if (k == 0) return c;
+  const std::size_t off = direction == ShiftDirection::Right ? k : m - k;
+  Chromosome out(m);
+  for (const std::size_t j : c.open_indices()) out.set((j + off) % m, true);
+  return out;
+}
+
+// Rotation of the subsequence [lo, hi] by k (ga.cpp:77-90).
+inline Chromosome block_shift(const Chromosome& c, std::size_t lo, std::size_t hi, std::size_t k,
+                              ShiftDirection direction) {
+  if (lo > hi || hi >= c.size()) throw DomainError("subsequence bounds out of range");
+  const std::size_t len = hi - lo + 1;
+  if (k >= len) throw DomainError("shift distance must not exceed the subsequence span");
+  if (k == 0) return c;
+  const std::size_t off = direction == ShiftDirection::Right ? k : len - k;
+  Chromosome out = c;
+  for (std::size_t t = 0; t < len; ++t) out.set(lo + (t + off) % len, c.test(lo + t));
+  return out;
+}
+
+// One mutation with the reference's draw order (ga.cpp:92-104): coin(whole),
+// coin(direction: true = Left), then k, or a, b, k.
+inline Chromosome random_shift_mutation(const Chromosome& c, RandomStream& rng) {
+  const std::size_t m = c.size();
+  const bool whole = rng.coin();
+  const ShiftDirection dir = rng.coin() ? ShiftDirection::Left : ShiftDirection::Right;
+  if (whole) return circular_shift(c, 1 + rng.below(m - 1), dir);
+  const std::size_t a = rng.below(m);
+  std::size_t b = rng.below(m - 1);
+  if (b >= a) ++b;
+  const std::size_t lo = a < b ? a : b, hi = a < b ? b : a;
+  return block_shift(c, lo, hi, rng.below(hi - lo + 1), dir);
+}
+
+// Partner of `thread` in a crossover round (ga.cpp:106-111): t XOR (nt >> (round + 1)).
+inline std::size_t crossover_couple(std::size_t thread, std::size_t round, std::size_t nt) {
+  const std::size_t sub = nt >> round, stride = sub / 2;
+  return thread % sub >= stride ? thread - stride : thread + stride;
+}
+
+// (cost, index) minimum, ties to the lower index (ga.cpp:113-134).
+inline std::pair<std::int64_t, std::size_t> block_min_reduce(std::span<const std::int64_t> costs) {
+  const std::size_t nt = costs.size();
+  if (nt == 0 || (nt & (nt - 1)) != 0) throw DomainError("reduction size must be a power of two");
+  std::size_t best = 0;
+  for (std::size_t t = 1; t < nt; ++t)
+    if (costs[t] < costs[best]) best = t;
+  return {costs[best], best};
+}
 
 namespace detail {
 inline pm_ga_config to_device(const GaConfig& cfg) {

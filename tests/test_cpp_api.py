@@ -52,11 +52,11 @@ def test_compat_api_runs(tmp_path):
 
 @pytest.mark.gpu
 def test_reference_unit_tests_pass_on_the_device():
-    """The reference's own test_chromosome / test_instance / test_formulation,
-    compiled unchanged against the compat headers by `make reftests` (where
-    /root/reference exists; the binary travels with the snapshot): every case
-    passes with build_ordering / fitness / min_cost_sum / exact_optimum_small on
-    the GPU."""
+    """The reference's own test_chromosome / test_instance / test_formulation /
+    test_ga (58 cases), compiled unchanged against the compat headers by `make
+    reftests` (where /root/reference exists; the binary travels with the
+    snapshot): every case passes with build_ordering / fitness / min_cost_sum /
+    exact_optimum_small / evolve_block / run_ga on the GPU."""
     exe = os.path.join(ROOT, "tests", "cpp", "_ref", "ref_tests")
     if not os.path.exists(exe):
         pytest.skip("tests/cpp/_ref/ref_tests not built (no /root/reference at build time)")
