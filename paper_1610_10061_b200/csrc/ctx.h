@@ -79,6 +79,7 @@ struct HostBuf {
 struct GaBuffers {
   DevBuf pop, next, cost, before, child, ccost, ok, brec, evals, tmp, table, ranks, rflags, rstate;
   DevBuf lfact;  // ln x! for x <= m + 1 (double): the unranking's search guide
+  size_t tab_m = 0, tab_p = 0, tab_L = 0;  // what `table` / `lfact` hold (0: nothing)
   HostBuf hrec, hmig;
 };
 }  // namespace pmb

@@ -784,7 +784,12 @@ struct HostDraw {
     // table entries C(x, y), x < m, y <= p, are at most C(m-1, min(p, (m-1)/2));
     // ranks are < C(m, p)
     const size_t L0 = std::max(binomial(m - 1, std::min(p, (m - 1) / 2)).limbs(), bound.limbs()) + 1;
-    if (L0 <= 32 && (m * (p + 1) + 1) * L0 * 8 <= (size_t)256 << 20) L = L0;
+    // device unranking while the Pascal table fits the budget (default 2 GiB of
+    // the 180 GB: syn20k's 20000 x 201 x 27 limbs take 0.87 GB); PMB_PASCAL_MAX_MB
+    // lowers it (tests force the host unranking path with it)
+    const char* cap_env = std::getenv("PMB_PASCAL_MAX_MB");
+    const size_t cap = (cap_env ? (size_t)std::atoll(cap_env) : (size_t)2048) << 20;
+    if (L0 <= 32 && (m * (p + 1) + 1) * L0 * 8 <= cap) L = L0;
   }
   void draw(size_t total, size_t lo, size_t hi, uint64_t* out /* (hi-lo) x wp */) {
     std::vector<UBig> ranks;
@@ -885,19 +890,27 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
     hd.init(cfg->seed, s.m, s.p);
     host_pop.resize(count * wp);
   }
-  if (ref_draw && hd.L) {  // the Pascal table for device unranking, once per run
+  if (ref_draw && hd.L && !(B.tab_m == (size_t)s.m && B.tab_p == (size_t)s.p && B.tab_L == hd.L)) {
+    // the Pascal table for device unranking: built and uploaded once per
+    // (m, p, limbs), kept across runs
+    B.tab_m = B.tab_p = B.tab_L = 0;
     const std::vector<uint64_t> tab = binomial_table(s.m, s.p, hd.L);
     PM_CUDA_TRY(c, B.table.ensure(tab.size() * 8));
     std::vector<double> lfact((size_t)s.m + 2);  // ln x!, the search guide of k_unrank_log
     for (size_t x = 0; x < lfact.size(); ++x) lfact[x] = std::lgamma((double)x + 1.0);
     PM_CUDA_TRY(c, B.lfact.ensure(lfact.size() * 8));
     PM_CUDA_TRY(c, cudaMemcpyAsync(B.lfact.p, lfact.data(), lfact.size() * 8, cudaMemcpyHostToDevice, c->stream));
-    PM_CUDA_TRY(c, B.ranks.ensure(count * hd.L * 8));
     // stream-ordered upload: a plain cudaMemcpy runs on the legacy stream, which
     // does not order against the context's non-blocking streams (the first
     // draw could read a partly written table)
     PM_CUDA_TRY(c, cudaMemcpyAsync(B.table.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
     PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // `tab` is freed at the end of this block
+    B.tab_m = (size_t)s.m;
+    B.tab_p = (size_t)s.p;
+    B.tab_L = hd.L;
+  }
+  if (ref_draw && hd.L) {
+    PM_CUDA_TRY(c, B.ranks.ensure(count * hd.L * 8));
     PM_CUDA_TRY(c, B.rstate.ensure(24));  // {position (even gen), position (odd gen), shortfall}
     PM_CUDA_TRY(c, cudaMemsetAsync(B.rstate.p, 0, 24, c->stream));
   }

@@ -161,11 +161,14 @@ def test_run_ga_device_population(ctx, pm, oracle):
     assert oracle.direct_cost(200, 200, 20, costs, a["best"]) == (0, a["best_cost"])
 
 
-@pytest.mark.parametrize("npts,p", [(1500, 150), (2200, 330), (2600, 520)])
-def test_run_ga_wide_ranks_match_reference(ctx, pm, oracle, reflib, npts, p):
-    """Population draws whose ranks need 12 / 22 limbs (the device unranking's
-    16- and 32-limb kernels) and 31 limbs (Pascal table over 256 MB: host
-    unranking), against the reference's own draw."""
+@pytest.mark.parametrize("npts,p,cap_mb", [(1500, 150, None), (2200, 330, None), (2600, 520, None),
+                                           (2600, 520, "256")])
+def test_run_ga_wide_ranks_match_reference(ctx, pm, oracle, reflib, npts, p, cap_mb, monkeypatch):
+    """Population draws whose ranks need 12 / 22 / 31 limbs (the device
+    unranking's 16- and 32-limb kernels) and, with the Pascal-table budget cut
+    to 256 MB, the host unranking path -- against the reference's own draw."""
+    if cap_mb:
+        monkeypatch.setenv("PMB_PASCAL_MAX_MB", cap_mb)
     costs = oracle.synth_euclid(npts)
     ctx.set_instance(costs, npts, npts, p)
     ri = reflib.create(npts, npts, p, costs)
