@@ -43,6 +43,20 @@ namespace pmb {
 
 size_t scan_t_stride(int m) { return ((size_t)m + 1 + 1) / 2 * 2; }
 
+// 32 x 32 bit-matrix transpose across a warp: lane L holds row L (bit b =
+// element (L, b)); on return lane L holds column L (bit b = element (b, L)).
+__device__ __forceinline__ uint32_t transpose32(int lane, uint32_t x) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int j = 16 >> i;
+    const uint32_t m = masks[i];
+    const uint32_t y = __shfl_xor_sync(kFull, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
 __global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __restrict__ words,
                                                               size_t count, int wp, int m,
                                                               uint64_t* __restrict__ T,
@@ -62,18 +76,11 @@ __global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __
   const size_t c0 = g * 64 + lane, c1 = c0 + 32;
   const uint64_t x = c0 < count ? words[c0 * wp + wi] : 0;
   const uint64_t y = c1 < count ? words[c1 * wp + wi] : 0;
-  uint64_t t0 = 0, t1 = 0;
-#pragma unroll
-  for (int b = 0; b < 32; ++b) {
-    const uint32_t lo0 = __ballot_sync(kFull, (x >> b) & 1);
-    const uint32_t hi0 = __ballot_sync(kFull, (y >> b) & 1);
-    const uint32_t lo1 = __ballot_sync(kFull, (x >> (b + 32)) & 1);
-    const uint32_t hi1 = __ballot_sync(kFull, (y >> (b + 32)) & 1);
-    if (lane == b) {
-      t0 = (uint64_t)lo0 | ((uint64_t)hi0 << 32);
-      t1 = (uint64_t)lo1 | ((uint64_t)hi1 << 32);
-    }
-  }
+  // four 32 x 32 bit transposes (butterfly over the lanes: 5 shuffle stages
+  // each): lane L ends with bit c = chromosome c opens site 64 wi + L (+ 32)
+  const uint64_t t0 = (uint64_t)transpose32(lane, (uint32_t)x) | ((uint64_t)transpose32(lane, (uint32_t)y) << 32);
+  const uint64_t t1 =
+      (uint64_t)transpose32(lane, (uint32_t)(x >> 32)) | ((uint64_t)transpose32(lane, (uint32_t)(y >> 32)) << 32);
   const int s0 = wi * 64 + lane, s1 = s0 + 32;
   if (s0 < m) Tg[s0] = t0;
   if (s1 < m) Tg[s1] = t1;
