@@ -61,21 +61,25 @@ __global__ void k_crossover_children(const uint64_t* __restrict__ before, uint64
   ok[idx] = success;
 }
 
-__global__ void k_crossover_accept(uint64_t* __restrict__ pop, int64_t* __restrict__ cost,
-                                   const uint64_t* __restrict__ child, const int64_t* __restrict__ ccost,
-                                   const uint8_t* __restrict__ ok, int count, int wp,
-                                   unsigned long long* __restrict__ evals) {
+// Accept into the other population buffer: nxt = child where it improved,
+// else the parent (ga.cpp:165-167), so the next round reads nxt as its
+// snapshot `before` and no copy of the population is needed between rounds.
+__global__ void k_crossover_accept_pp(const uint64_t* __restrict__ cur, uint64_t* __restrict__ nxt,
+                                      int64_t* __restrict__ cost, const uint64_t* __restrict__ child,
+                                      const int64_t* __restrict__ ccost, const uint8_t* __restrict__ ok, int count,
+                                      int wp, unsigned long long* __restrict__ evals) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long e = 0;
-  if (idx < count && ok[idx]) {
-    e = 1;  // the reference evaluates every successful child (ga.cpp:166)
-    if (ccost[idx] < cost[idx]) {
-      for (int w = 0; w < wp; ++w) pop[(size_t)idx * wp + w] = child[(size_t)idx * wp + w];
-      cost[idx] = ccost[idx];
-    }
+  unsigned e = 0;
+  if (idx < count) {
+    const bool success = ok[idx];
+    e = success;  // the reference evaluates every successful child (ga.cpp:166)
+    const bool take = success && ccost[idx] < cost[idx];
+    const uint64_t* src = (take ? child : cur) + (size_t)idx * wp;
+    for (int w = 0; w < wp; ++w) nxt[(size_t)idx * wp + w] = src[w];
+    if (take) cost[idx] = ccost[idx];
   }
-  e = __reduce_add_sync(0xffffffffu, (unsigned)e);
-  if ((threadIdx.x & 31) == 0 && e) atomicAdd(evals, e);
+  e = __reduce_add_sync(0xffffffffu, e);
+  if ((threadIdx.x & 31) == 0 && e) atomicAdd(evals, (unsigned long long)e);
 }
 
 __global__ void k_mutation_children(const uint64_t* __restrict__ pop, uint64_t* __restrict__ child,
@@ -672,19 +676,27 @@ static int evolve_all(pm_ctx* c, GaBuffers& B, const GaShape& s, uint64_t kernel
   int rc = evaluate_core(c, pop, count, cost, 0);  // ga.cpp:146-147
   if (rc) return rc;
   if (s.p >= 2) {  // ga.cpp:154
+    // ping-pong between pop and before: a round reads its snapshot `cur` and
+    // the accept writes the next round's population into `nxt`
+    uint64_t* cur = pop;
+    uint64_t* nxt = B.before.as<uint64_t>();
     for (int r = 0; r < s.rounds; ++r) {
-      PM_CUDA_TRY(c, cudaMemcpyAsync(B.before.p, pop, count * s.wp * 8, cudaMemcpyDeviceToDevice, c->stream));
       k_crossover_children<<<cdiv(count, tb), tb, 0, c->stream>>>(
-          B.before.as<uint64_t>(), B.child.as<uint64_t>(), B.ok.as<uint8_t>(), s.nbl, s.nt, s.wp, s.m, s.p,
-          s.seed, kernel, s.block0, (uint64_t)r, s.cycle);
+          cur, B.child.as<uint64_t>(), B.ok.as<uint8_t>(), s.nbl, s.nt, s.wp, s.m, s.p, s.seed, kernel, s.block0,
+          (uint64_t)r, s.cycle);
       PM_CUDA_TRY(c, cudaGetLastError());
       rc = evaluate_core(c, B.child.as<uint64_t>(), count, B.ccost.as<int64_t>(), 0);
       if (rc) return rc;
-      k_crossover_accept<<<cdiv(count, tb), tb, 0, c->stream>>>(pop, cost, B.child.as<uint64_t>(),
-                                                                 B.ccost.as<int64_t>(), B.ok.as<uint8_t>(),
-                                                                 (int)count, s.wp, evals);
+      k_crossover_accept_pp<<<cdiv(count, tb), tb, 0, c->stream>>>(cur, nxt, cost, B.child.as<uint64_t>(),
+                                                                    B.ccost.as<int64_t>(), B.ok.as<uint8_t>(),
+                                                                    (int)count, s.wp, evals);
       PM_CUDA_TRY(c, cudaGetLastError());
       c->launches += 2;
+      std::swap(cur, nxt);
+    }
+    if (cur != pop) {  // an odd round count left the population in `before`
+      std::swap(B.pop, B.before);
+      pop = B.pop.as<uint64_t>();
     }
   }
   if (s.attempts > 0) {
