@@ -106,16 +106,41 @@ __global__ void __launch_bounds__(256) k_mutation_children_wide(const uint64_t* 
                                                                 int wp, int m, uint64_t seed, uint64_t kernel,
                                                                 uint64_t block0, int attempts) {
   extern __shared__ ShiftDraw sd[];  // [32][attempts]
+  __shared__ int redo[32];           // a rejection shifted the stream: redraw sequentially
   const int count = nbl * nt;
   const int c0 = blockIdx.x * 32;
-  if (threadIdx.x < 32) {
-    const int idx = c0 + threadIdx.x;
-    if (idx < count) {
-      const int b = idx / nt, t = idx % nt;
-      const uint64_t key[4] = {kMutationTag, kernel, block0 + b, (uint64_t)t};
-      Stream rng = Stream::derive(seed, key, 4);
-      for (int a = 0; a < attempts; ++a) sd[threadIdx.x * attempts + a] = draw_shift(m, rng);
+  if (threadIdx.x < 32) redo[threadIdx.x] = 0;
+  __syncthreads();
+  // Every (chromosome, attempt) draws in parallel.  An attempt consumes 2 coins
+  // plus 1 (whole rotation) or 3 (sub-range) bounded draws, one output each
+  // unless a draw rejects (probability < 2^-47 per draw at these bounds), so a
+  // task finds its attempt's stream position from the earlier attempts' first
+  // coins alone; a task whose own draw rejected flags its chromosome, which
+  // is then redrawn sequentially -- exact in every case.
+  constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+  for (int task = threadIdx.x; task < 32 * attempts; task += blockDim.x) {
+    const int cl = task / attempts, a = task - cl * attempts;
+    const int idx = c0 + cl;
+    if (idx >= count) continue;
+    const int b = idx / nt, t = idx % nt;
+    const uint64_t key[4] = {kMutationTag, kernel, block0 + b, (uint64_t)t};
+    Stream rng = Stream::derive(seed, key, 4);
+    for (int q = 0; q < a; ++q) {
+      const bool whole = rng.coin();
+      rng.state += (whole ? 2 : 4) * kGamma;  // direction coin + 1 or 3 draws
     }
+    const uint64_t before = rng.state;
+    const bool whole = (mix64(before + kGamma) & 1) != 0;  // this attempt's first coin
+    sd[cl * attempts + a] = draw_shift(m, rng);
+    if (rng.state != before + (whole ? 3 : 5) * kGamma) redo[cl] = 1;  // a draw rejected
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && redo[threadIdx.x]) {
+    const int idx = c0 + threadIdx.x;
+    const int b = idx / nt, t = idx % nt;
+    const uint64_t key[4] = {kMutationTag, kernel, block0 + b, (uint64_t)t};
+    Stream rng = Stream::derive(seed, key, 4);
+    for (int a = 0; a < attempts; ++a) sd[threadIdx.x * attempts + a] = draw_shift(m, rng);
   }
   __syncthreads();
   const int nc = min(32, count - c0);
