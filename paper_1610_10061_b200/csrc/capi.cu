@@ -32,14 +32,19 @@ int pm_create(int device, pm_ctx** out) {
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   c->max_smem = (size_t)optin;
-  if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+  // the context's stream at the highest priority: the GA's population draw
+  // for the next generation (draw_stream, default priority) fills the SMs the
+  // evolution leaves idle instead of delaying it
+  int prio_least = 0, prio_greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
+  if (cudaStreamCreateWithPriority(&c->own, cudaStreamNonBlocking, prio_greatest) != cudaSuccess) {
     delete c;
     return PM_CUDA;
   }
   c->stream = c->own;
   if (c->errw.ensure(kErrSlots * 8) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->draw_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->draw_stream, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->draw_ev, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return PM_CUDA;
