@@ -27,6 +27,18 @@ $(CLI): $(PKG)/cli/pmedian_bench.cpp $(LIB) $(PKG)/csrc/combinatorics.h
 oracle:
 	$(MAKE) -s -C oracle
 
+# Bounds-checked variant (-DPMB_BOUNDS: device PMB_CHECKs trap on an index outside
+# its buffer); same sources, loaded with PMB_LIBRARY=$(BOUNDS_LIB) by
+# tools/bounds_check.py and the GPU test suite.  Not part of `all`.
+BOUNDS_OBJS := $(patsubst $(PKG)/csrc/%.cu,build_bounds/%.o,$(CSRC))
+BOUNDS_LIB  := $(PKG)/libpmedian_b200_bounds.so
+build_bounds/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/pmedian_b200.h
+	@mkdir -p build_bounds
+	$(NVCC) $(NVFLAGS) -DPMB_BOUNDS -c $< -o $@
+$(BOUNDS_LIB): $(BOUNDS_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(BOUNDS_OBJS) -lcudart_static -lrt -ldl -lpthread
+bounds: $(BOUNDS_LIB)
+
 # TEST INFRASTRUCTURE: the reference's own unit tests (test_chromosome,
 # test_instance, test_formulation, test_ga) compiled unchanged against the compat
 # headers (include/compat/pmedian/ -> the device path) with a doctest stand-in.
@@ -42,7 +54,7 @@ reftests: $(LIB)
 	else echo "reftests: $(REF_TESTS_DIR) absent, keeping prebuilt $(REFTESTS) (if any)"; fi
 
 clean:
-	rm -rf build $(LIB) $(CLI)
+	rm -rf build build_bounds $(LIB) $(BOUNDS_LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle reftests clean
+.PHONY: all oracle reftests clean bounds

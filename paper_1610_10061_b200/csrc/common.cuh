@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #ifndef __CUDACC__
 #error "common.cuh is CUDA-only"
@@ -11,6 +12,26 @@
 namespace pmb {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// Device bounds checks for the `make bounds` build (-DPMB_BOUNDS): an index
+// outside its buffer prints the kernel's source line and traps, so a bad
+// access surfaces as a CUDA error instead of a wrong cost.  (compute-sanitizer
+// is not available on the GPU pool; tools/bounds_check.py drives this build.)
+// The release build compiles every check away.
+#ifdef PMB_BOUNDS
+#define PMB_CHECK(cond)                                                                             \
+  do {                                                                                              \
+    if (!(cond)) {                                                                                  \
+      printf("PMB_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,        \
+             (int)blockIdx.x, (int)threadIdx.x);                                                    \
+      __trap();                                                                                     \
+    }                                                                                               \
+  } while (0)
+#else
+#define PMB_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ unsigned lanemask_lt() {

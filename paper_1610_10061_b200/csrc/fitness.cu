@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
         const int avail = wb_end - wb_next;
         if (i < 0 && rank < avail) {
           i = wb_next + rank;
+          PMB_CHECK(i >= c0 && i < c1 && c1 <= n);
           k = 0;
           alive = vmask;
           orow = ord + (size_t)i * Wp;
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
       MaskT t[kChunk];
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
+        PMB_CHECK(cur.site(j) < Ts);
         if constexpr (kTSmem) t[j] = Tsm[cur.site(j)];
         else t[j] = (MaskT)(__ldg(Tg + cur.site(j)) >> half);
       }
@@ -346,6 +348,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
           // (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
           const AccT dval = kDepth ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
           const uint32_t q = qn + __popc(hb & lt);
+          PMB_CHECK(q < (uint32_t)kQ);
           if constexpr (kPacked) {
             wq[q] = (uint64_t)h | ((uint64_t)dval << 32);
           } else {
@@ -366,6 +369,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
           nxt.set_sentinel(sentinel);
           nxt2.set_sentinel(sentinel);
         } else if (k + (kBufs - 1) * kChunk < Wp) {
+          PMB_CHECK(k + kBufs * kChunk <= Wp);
           cur.load(orow, drow, k + (kBufs - 1) * kChunk);
         }
       }
@@ -669,8 +673,12 @@ __global__ void __launch_bounds__(kGatherThreads)
       if (nv > 0) {
         const uint32_t* list = lists + c * (size_t)cap;
         uint32_t t = 0;
+        PMB_CHECK(i0 + V <= nP && pc <= (uint32_t)cap);
         for (; t + 4 <= pc; t += 4) {
           uint4 x[4];
+#ifdef PMB_BOUNDS
+          for (int u = 0; u < 4; ++u) PMB_CHECK(list[t + u] < (uint32_t)m);
+#endif
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             x[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)__ldg(list + t + u) * nP));

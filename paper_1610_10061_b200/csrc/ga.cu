@@ -52,6 +52,7 @@ __global__ void k_crossover_children(const uint64_t* __restrict__ before, uint64
   Stream rng = Stream::derive(seed, key, 5);
   const int start = (int)rng.below((uint64_t)m);
   const int exchanges = 2 * (1 + (int)rng.below((uint64_t)(p / 2)));
+  PMB_CHECK(couple < (uint32_t)nt && start >= 0 && start < m && exchanges <= p);
   const uint64_t* a = before + (size_t)idx * wp;
   const uint64_t* bb = before + ((size_t)b * nt + couple) * wp;
   uint64_t* c = child + (size_t)idx * wp;
