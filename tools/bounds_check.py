@@ -91,7 +91,7 @@ def main():
             text = random_graph(5, 60, 90, oracle=o)
             ctx.set_instance_orlib(text, p=6)
             print("orlib ok", flush=True)
-    print("sanitize driver ok")
+    print(f"bounds driver ok ({pm.LIB_PATH})")
 
 
 if __name__ == "__main__":
