@@ -98,6 +98,11 @@ cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int
 
 constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
 constexpr int kWideWarps = 24, kWideQueue = 256;  // the many-warp K2 variant (plan_scan)
+#ifndef PMB_QCHECK
+#define PMB_QCHECK 2
+#endif
+constexpr int kQCheck = PMB_QCHECK;  // columns between queue-overflow checks (many-warp variant)
+static_assert(16 % kQCheck == 0 && kWideQueue > 32 * kQCheck, "queue check stride");
 
 template <class OrdT, class DistT>
 struct Chunk {
@@ -335,7 +340,8 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
         if constexpr (kQ < kChunk * 32) {
-          if (qn > (uint32_t)(kQ - 32)) {  // warp-uniform: the next column could overflow
+          // every kQCheck columns (warp-uniform): the next kQCheck columns could overflow
+          if (j % kQCheck == 0 && qn > (uint32_t)(kQ - 32 * kQCheck)) {
             drain(qn);
             qn = 0;
           }
