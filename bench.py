@@ -8,9 +8,11 @@ population (the batch evolve_block hands to fitness(), ga.cpp:147).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config syn20k|syn5k|sweep:P|pmed40]
   python bench.py --impl reference ...   # the reference's own fitness() on the host cores
 
-Under torchrun (N>1) every rank evaluates its own 4096-chromosome shard of a
-global population against locally built, replicated tables: weak scaling, no
-data-path collective; only the timing max-reduction crosses ranks.
+Under torchrun (N>1) the BASELINE population is split contiguously over the
+ranks (BASELINE configs 3-4: one batch, strong scaling), every rank evaluates
+its shard against locally built, replicated tables, and the costs are
+all-gathered (NCCL) inside the timed step; `--scaling weak` gives every rank a
+whole population of its own instead.
 
 Timing: W warm-up steps, then K steps; before every timed step a 512 MiB
 buffer is written to flush L2; each step is bracketed by CUDA events on the
@@ -148,6 +150,19 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def allgather_into(dst, src):
+    """dst (world * len(src)) <- every rank's src, in rank order.  NCCL on the
+    device tensors; over gloo (CPU plumbing tests) through host copies."""
+    import torch
+    import torch.distributed as dist
+    if BACKEND == "nccl":
+        dist.all_gather_into_tensor(dst, src)
+        return
+    parts = [torch.empty_like(src, device="cpu") for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, src.cpu())
+    dst.copy_(torch.cat(parts))
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -165,14 +180,52 @@ def cpu_model():
     return None
 
 
-def cpu_reference_sample(site_order, increments, n, m, p, words, gpu_costs, budget_s=10.0):
-    """The reference's own fitness() (oracle/_ref, compiled from /root/reference sources)
-    on all host threads over a bounded sample of the same population."""
+def load_synth():
+    """paper_1610_10061_b200/synth.py loaded by path: the reference arm must not
+    import the package (whose __init__ maps libpmedian_b200.so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("pmb_synth", os.path.join(ROOT, "paper_1610_10061_b200", "synth.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def source_hash(*rel):
+    import hashlib
+    h = hashlib.sha256()
+    for r in rel:
+        with open(os.path.join(ROOT, r), "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_record(config: str, kernel: str):
+    """The committed ncu --set full summary of the dominant kernel
+    (profiles/ncu_<kernel>_<config>.json, tools/ncu_to_json.py), stamped with the
+    hash of the kernel source it was captured from; `stale` when the source
+    changed since."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{kernel}_{config}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        rec = json.load(f)
+    rec["stale"] = rec.get("source_sha16") != source_hash("paper_1610_10061_b200/csrc/fitness.cu")
+    rec["file"] = os.path.relpath(path, ROOT)
+    return rec
+
+
+def cpu_reference_sample(costs_host, n, m, p, words, gpu_costs, budget_s=10.0):
+    """The reference's own build_ordering + fitness() (oracle/_ref, compiled from
+    /root/reference sources) on all host threads over a bounded sample of the
+    same population, on the reference's OWN tables (so the GPU costs are checked
+    end to end: K1 and K2)."""
     from oracle.oracle import RefLib
     if not RefLib.available():
         return None
     ref = RefLib()
-    ri = ref.create_with_tables(n, m, p, site_order, increments)
+    t0 = time.perf_counter()
+    ri = ref.create(n, m, p, costs_host)  # Instance + build_ordering (single thread, ordering.cpp:10-38)
+    build_s = time.perf_counter() - t0
     threads = len(os.sched_getaffinity(0))
     probe = words[:threads]
     t0 = time.perf_counter()
@@ -192,9 +245,19 @@ def cpu_reference_sample(site_order, increments, n, m, p, words, gpu_costs, budg
     ri.evaluate(words[:one], 1)
     dt1 = time.perf_counter() - t0
     return {"value": count / dt, "unit": "evals/s", "cores": threads, "kind": "reference",
-            "sample": f"first {count} chromosomes of the same population, reference fitness() "
-                      f"(proj/src/ordering.cpp:40-59) on {threads} host threads, {dt:.1f} s",
-            "bit_exact_vs_gpu": parity, "single_thread_value": one / dt1, "cpu_model": cpu_model()}
+            "sample": f"first {count} of the {words.shape[0]} chromosomes of the same population, reference "
+                      f"fitness() (proj/src/ordering.cpp:40-59) on the reference's own build_ordering tables, "
+                      f"{threads} host threads, {dt:.1f} s",
+            "bit_exact_vs_gpu": parity, "single_thread_value": one / dt1,
+            "reference_build_ordering_s": round(build_s, 2), "cpu_model": cpu_model()}
+
+
+def workload_config(cfg, n, m, p, world, scaling):
+    """The `config` object: workload-defining keys only, identical in both arms."""
+    count = cfg["count"]
+    total = count if scaling == "strong" else count * world
+    return {"workload": cfg["workload"], "n": n, "m": m, "p": p, "population": total,
+            "scaling": scaling, "instance_seed": 12345, "population_seed": 7}
 
 
 def run_ours(args):
@@ -210,6 +273,9 @@ def run_ours(args):
     n = m = cfg["npts"]
     p, count = cfg["p"], cfg["count"]
     wp = (m + 63) // 64
+    scaling = args.scaling
+    if scaling == "strong" and count % world:
+        raise SystemExit(f"strong scaling needs the population ({count}) divisible by {world}")
 
     ctx = pm.Context(local)
     stream = torch.cuda.current_stream(dev)
@@ -225,19 +291,50 @@ def run_ours(args):
     del costs
     torch.cuda.empty_cache()
 
-    pop = synth.random_population(m, p, count, seed=7 + 1000 * rank)  # this rank's shard
-    words_host = torch.from_numpy(pop.view(np.int64)).pin_memory()
+    # strong: one global population (seed 7), contiguous shard per rank, costs
+    # all-gathered back; weak: every rank its own population of `count`
+    if scaling == "strong":
+        pop_all = synth.random_population(m, p, count, seed=7)
+        per = count // world
+        pop = pop_all[rank * per:(rank + 1) * per]
+    else:
+        pop_all = None
+        per = count
+        pop = synth.random_population(m, p, count, seed=7 + 1000 * rank)
+    words_host = torch.from_numpy(np.ascontiguousarray(pop).view(np.int64)).pin_memory()
     words = words_host.to(dev)
-    out = torch.empty(count, dtype=torch.int64, device=dev)
-    sumk = torch.empty(count, dtype=torch.int64, device=dev)
-    ctx.scan_depths_device(words, sumk, count, wp)
-    algo_bytes = 12 * int(sumk.sum().item()) + 8 * wp * count  # SURVEY.md 8(d) B_eval x count
+    out = torch.empty(per, dtype=torch.int64, device=dev)
+    gathered = torch.empty(per * world, dtype=torch.int64, device=dev) if scaling == "strong" else None
+    sumk = torch.empty(per, dtype=torch.int64, device=dev)
+    ctx.scan_depths_device(words, sumk, per, wp)
+    algo_bytes = 12 * int(sumk.sum().item()) + 8 * wp * per  # SURVEY.md 8(d) B_eval x shard
+    ti = ctx.table_info()
+    col_bytes = ti.site_bytes + ti.dist_bytes
+    gsum = torch.zeros((per + 31) // 32, dtype=torch.int64, device=dev)
+    cmax = torch.zeros(n, dtype=torch.int32, device=dev)
+    ctx.scan_walks_device(words, gsum, cmax, per, wp)
+    group_stream_bytes = int(gsum.sum().item()) * col_bytes
+    ts = (m + 2) // 2 * 2
+    dram_floor_bytes = int(cmax.to(torch.int64).sum().item()) * col_bytes + ((per + 63) // 64) * ts * 8 + per * 8
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
+    def gather_costs():
+        if gathered is not None and world > 1:
+            allgather_into(gathered, out)
+
     for _ in range(args.warmup):
-        ctx.evaluate_device(words, out, count, wp, check=False)
+        ctx.evaluate_device(words, out, per, wp, check=False)
+        gather_costs()
     ctx.check_errors()
     gpu_costs = out.cpu().numpy()
+    if scaling == "strong":
+        # the split is exact: the gathered costs equal one evaluation of the whole batch
+        full = torch.empty(count, dtype=torch.int64, device=dev)
+        wfull = torch.from_numpy(np.ascontiguousarray(pop_all).view(np.int64)).to(dev)
+        ctx.evaluate_device(wfull, full, count, wp, check=True)
+        if world > 1:
+            assert torch.equal(gathered, full), "strong split: gathered costs differ from the whole-batch result"
+        del wfull
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -250,7 +347,8 @@ def run_ours(args):
         for s in range(args.steps):
             flush.zero_()
             starts[s].record(stream)
-            ctx.evaluate_device(words, out, count, wp, check=False)
+            ctx.evaluate_device(words, out, per, wp, check=False)
+            gather_costs()
             ends[s].record(stream)
         torch.cuda.synchronize()
     barrier(world)
@@ -260,47 +358,68 @@ def run_ours(args):
     ctx.check_errors()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     total_ms = max_over_ranks(float(sum(step_ms)), world)
-    value = count * world * args.steps / (total_ms / 1e3)
+    units = count if scaling == "strong" else count * world
+    value = units * args.steps / (total_ms / 1e3)
 
-    # e2e: the public host-buffer call (pm_evaluate) with H2D of the population
-    # from pinned memory and D2H of the costs inside the timed region
+    # e2e: the public host-buffer call (pm_evaluate) with the H2D of this rank's
+    # chromosomes from pinned memory and the D2H of its costs (and, strong, the
+    # all-gather of the costs) inside a host wall-clock bracket per step
     host_pop = words_host.numpy().view(np.uint64)
     for _ in range(2):
         ctx.evaluate(host_pop)
-    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e2e_s = []
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk2:
         for s in range(args.steps):
             flush.zero_()
-            e_s[s].record(stream)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
             res = ctx.evaluate(host_pop)
-            e_e[s].record(stream)
-        torch.cuda.synchronize()
+            if scaling == "strong" and world > 1:
+                g = torch.empty(per * world, dtype=torch.int64, device=dev)
+                allgather_into(g, torch.from_numpy(res).to(dev))
+                res_all = g.cpu().numpy()
+                assert res_all.shape[0] == count
+            e2e_s.append(time.perf_counter() - t0)
     barrier(world)
     assert (res == gpu_costs).all()
-    e2e_ms = max_over_ranks(float(sum(a.elapsed_time(b) for a, b in zip(e_s, e_e))), world)
-    e2e_value = count * world * args.steps / (e2e_ms / 1e3)
+    e2e_total = max_over_ranks(float(sum(e2e_s)), world)
+    e2e_value = units * args.steps / e2e_total
 
     peak, peak_src = peaks()
     avg_kernel_s = kern_ms / max(1, kern_n) / 1e3
     achieved = algo_bytes / avg_kernel_s / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get(args.config)
-    kernel_name = "k_scan (K2, bit-sliced scan)" if ctx.auto_eval_kernel() == 1 and args.kernel != "gather" \
-        else "k_gather (K2b, gather-min)"
-    if args.kernel == "scan":
-        kernel_name = "k_scan (K2, bit-sliced scan)"
+    kname = "k_scan" if (ctx.auto_eval_kernel() == 1 and args.kernel == "auto") or args.kernel == "scan" \
+        else "k_gather"
+    kernel_name = {"k_scan": "k_scan (K2, bit-sliced scan)", "k_gather": "k_gather (K2b, gather-min)"}[kname]
+    ncu = ncu_record(args.config, kname)
+    physical = {
+        "group_stream_bytes": group_stream_bytes,
+        "group_stream_gbs": group_stream_bytes / avg_kernel_s / 1e9,
+        "dram_floor_bytes": dram_floor_bytes,
+        "dram_floor_gbs": dram_floor_bytes / avg_kernel_s / 1e9,
+        "dram_floor_frac": dram_floor_bytes / avg_kernel_s / 1e9 / peak,
+        "definition": "measured in this run (pm_scan_walks_device): group_stream = sum over 32-chromosome "
+                      "groups and clients of the walk max_{c in group} k*_ic x (site+dist bytes) -- the row "
+                      "prefixes K2 must stream from L2; dram_floor = sum over clients of the longest walk x "
+                      "(site+dist bytes) + transposed masks + population + costs -- bytes that must come from "
+                      "DRAM at least once per launch",
+    }
+    if ncu:
+        physical["ncu_dram_bytes"] = ncu.get("dram_bytes")
+        physical["ncu_dram_frac"] = (ncu["dram_bytes"] / avg_kernel_s / 1e9 / peak) if ncu.get("dram_bytes") else None
+        physical["binding"] = {k: ncu.get(k) for k in ("l1tex_throughput_pct", "issue_active_pct",
+                                                         "sm_throughput_pct", "lts_throughput_pct",
+                                                         "dram_throughput_pct", "warp_instructions",
+                                                         "duration_ms")}
+        physical["ncu_source"] = {k: ncu.get(k) for k in ("file", "source_sha16", "stale", "commit", "captured")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        so, inc = ctx.get_tables()
-        cpu = cpu_reference_sample(so, inc, n, m, p, pop, gpu_costs, budget_s=args.cpu_seconds)
-        del so, inc
+        costs_host = synth.euclid_costs(n, 12345)
+        cpu = cpu_reference_sample(costs_host, n, m, p, pop, gpu_costs, budget_s=args.cpu_seconds)
+        del costs_host
 
     ga = None if args.no_ga else bench_ga(ctx, args, world, rank, local, n, m, p)
     evolved = None
@@ -317,26 +436,34 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "int64",
         "data": "synthetic (seeded Euclidean instance, uniform random p-subset population)",
-        "config": {"workload": cfg["workload"], "n": n, "m": m, "p": p, "population_per_gpu": count,
-                   "parallelism": f"population sharded over {world} GPU(s), tables replicated",
-                   "l2": "flushed before every timed step (512 MiB write)",
-                   "kernel": kernel_name, "build_ordering_s": round(build_s, 3)},
+        "config": workload_config(cfg, n, m, p, world, scaling),
+        "details": {"per_gpu_chromosomes": per,
+                    "parallelism": (f"one {count}-chromosome batch split contiguously over {world} GPU(s), "
+                                    "costs all-gathered (NCCL) inside the step" if scaling == "strong" else
+                                    f"{count} chromosomes per GPU, tables replicated, no data-path collective"),
+                    "l2": "flushed before every timed step (512 MiB write)",
+                    "kernel": kernel_name, "build_ordering_s": round(build_s, 3)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": ncu.get("dram_bytes") if ncu else None,
                      "kernel": kernel_name, "avg_kernel_ms": avg_kernel_s * 1e3,
                      "algorithmic_bytes_per_launch": algo_bytes,
                      "bytes_definition": "SURVEY.md 8(d): B_eval = 12*sum_i k*_i + 8*ceil(m/64) per "
                                          "chromosome (reference layout, no reuse); effective-bandwidth "
-                                         "figure, may exceed 1.0 -- see traffic for physical DRAM bytes",
+                                         "figure, may exceed 1.0 -- see `physical` for the reuse-aware floors "
+                                         "and the ncu-measured DRAM traffic and binding units",
+                     "physical": physical,
                      "peak_source": peak_src},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": count * wp * 8,
-                "d2h_bytes_per_step": count * 8,
-                "call": "pm_evaluate (C ABI, host buffers; population from pinned memory)"},
+        "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": per * wp * 8,
+                "d2h_bytes_per_step": per * 8,
+                "call": "pm_evaluate (C ABI, host buffers; population from pinned memory); host wall clock "
+                        "around each synchronous call" + (", plus the cost all-gather" if world > 1 and
+                                                          scaling == "strong" else ""),
+                "bytes_note": "per GPU per step"},
         "gpu_launches": launches,
         "clocks": clocks,
         "clocks_e2e": clk2.summary(),
@@ -361,10 +488,12 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
     import paper_1610_10061_b200 as pm
     from paper_1610_10061_b200 import synth
     out = {}
-    # syn20k-shape island GA: 16 blocks x 256 per GPU, islands over the ranks;
-    # the reference's exact population draw (device rank draw + unranking over
-    # a 0.87 GB Pascal table), then the device draw (same distribution)
-    nb = 16 * world
+    # syn20k-shape island GA (BASELINE config 4): 16 blocks x 256 = 4096
+    # chromosomes in total, split over the ranks as islands (strong; weak: 16
+    # blocks per GPU); the reference's exact population draw (device rank draw
+    # + unranking over a 0.87 GB Pascal table), then the device draw (same
+    # distribution)
+    nb = 16 * world if args.scaling == "weak" else 16
     ag = None
     if world > 1 and BACKEND == "nccl":
         # the library's own NCCL exchange (pm_nccl_*); torch.distributed only
@@ -381,7 +510,7 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
         warm = pm.ga_config(nb=nb, nt=256, evolve_limit=1, saturation=1, seed=2, population=pop_mode)
         ctx.run_ga(warm, rank=rank, world=world, allgather=ag)  # kernels loaded, Pascal table resident
         r = ctx.run_ga(cfg, rank=rank, world=world, allgather=ag)
-        out[key] = {"config": f"n=m={n}, p={p}, nb={nb} ({16} per GPU), nt=256, {pop_mode} population draw",
+        out[key] = {"config": f"n=m={n}, p={p}, nb={nb} ({nb // world} per GPU), nt=256, {pop_mode} population draw",
                     "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
                     "best_cost": r["best_cost"], "evals_per_gen_reference_semantics":
                         r["evaluations"] / r["kernels_executed"],
@@ -488,13 +617,16 @@ def exhaustive_optimum(ctx, m, p):
 
 
 def run_reference(args):
-    """--impl reference: the reference's own CPU fitness() (oracle/_ref) on the host cores."""
+    """--impl reference: the reference's own CPU build_ordering + fitness()
+    (oracle/_ref, compiled from /root/reference/proj/src) on all host cores, on
+    the SAME workload as the GPU arm: every step evaluates the whole
+    population.  Never imports the product package."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle.oracle import RefLib
-    from paper_1610_10061_b200 import synth
+    synth = load_synth()
     cfg = config_for(args.config)
     n = m = cfg["npts"]
     p, count = cfg["p"], cfg["count"]
@@ -508,10 +640,11 @@ def run_reference(args):
     build_s = time.perf_counter() - t0
     del costs
     threads = len(os.sched_getaffinity(0))
-    sample = max(threads, min(count, args.ref_sample or threads * 4) // threads * threads)
+    total = count if args.scaling == "strong" else count * world
+    sample = min(total, args.ref_sample) if args.ref_sample else total
     pop = synth.random_population(m, p, sample, seed=7)
     for _ in range(args.warmup):
-        ri.evaluate(pop[:threads], threads)
+        ri.evaluate(pop, threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
@@ -522,14 +655,15 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (seeded Euclidean instance, uniform random p-subset population)",
-        "config": {"workload": cfg["workload"], "n": n, "m": m, "p": p,
-                   "parallelism": f"{threads} host threads (std::thread slices, ga.cpp:253-277)",
-                   "build_ordering_s": round(build_s, 2),
-                   "step": f"reference fitness() over {sample} chromosomes of the population"},
+        "config": workload_config(cfg, n, m, p, world, args.scaling),
+        "details": {"parallelism": f"{threads} host threads (std::thread slices, ga.cpp:253-277)",
+                    "build_ordering_s": round(build_s, 2),
+                    "step": f"reference fitness() over {sample} chromosomes of the population",
+                    "cpu_model": cpu_model()},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
-                         "sample": f"{sample} chromosomes per step, {args.steps} steps"},
+                         "sample": f"{sample} chromosomes per step (the whole workload), {args.steps} steps"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     del ri
@@ -565,6 +699,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-ga", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default): the BASELINE population split over the GPUs; weak: per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -130,6 +130,13 @@ int pm_min_cost_sum(pm_ctx* ctx, const uint64_t* bitsets, size_t count, size_t w
  * buffers; synchronises; PM_CONTRACT as pm_evaluate on a runoff. */
 int pm_scan_depths_device(pm_ctx* ctx, const uint64_t* bitsets_device, size_t count,
                           size_t words_per, uint64_t* sum_k_device);
+/* The scan's reuse-aware work (measurement only): per 32-chromosome group g
+ * (ceil(count/32) entries) the sum over clients of walk_gi = max_{c in g} k*_ic
+ * -- the columns K2 walks once for the whole group -- and per client the
+ * maximum walk over all groups (n entries), i.e. the row prefix that must be
+ * read from DRAM at least once.  Device buffers; synchronises. */
+int pm_scan_walks_device(pm_ctx* ctx, const uint64_t* bitsets_device, size_t count, size_t words_per,
+                         uint64_t* group_walk_sum_device, uint32_t* client_max_walk_device);
 /* When enabled, CUDA events on the context stream bracket every launch of the
  * dominant evaluation kernel (K2 scan or K2b gather). */
 int pm_set_profiling(pm_ctx* ctx, int enabled);
@@ -197,8 +204,13 @@ int pm_evolve_blocks(pm_ctx* ctx, uint64_t* blocks, size_t nb, size_t words_per,
                      uint64_t kernel_index, size_t first_block, int64_t* best_cost, size_t* best_thread);
 
 /* Replaces pmedian::run_ga (ga.hpp:109) on the context's instance.  best_words
- * (ceil(m/64) words) receives RunResult::best, per_kernel_best (evolve_limit
- * entries) RunResult::per_kernel_best_costs. */
+ * (ceil(m/64) words) receives RunResult::best; per_kernel_best, if not NULL,
+ * receives RunResult::per_kernel_best_costs (kernels_executed <= evolve_limit
+ * entries).  A caller that cannot size a buffer by evolve_limit (a large limit
+ * that relies on saturation) passes NULL and reads them afterwards with
+ * pm_last_per_kernel_best.  The generation step -- global best, stop rule,
+ * migration (ga.cpp:279-297) -- runs on the device; the host reads one stop
+ * word per generation. */
 int pm_run_ga(pm_ctx* ctx, const pm_ga_config* cfg, uint64_t* best_words, int64_t* per_kernel_best,
               pm_run_result* result);
 
@@ -212,6 +224,21 @@ typedef int (*pm_allgather_fn)(const void* send, size_t bytes, void* recv, void*
 int pm_run_ga_islands(pm_ctx* ctx, const pm_ga_config* cfg, int rank, int world, pm_allgather_fn allgather,
                       void* user, uint64_t* best_words, int64_t* per_kernel_best, pm_run_result* result);
 
+/* The same with a DEVICE collective: `allgather` enqueues the gather of the
+ * device buffer `send_device` (bytes) into `recv_device` (world * bytes, rank
+ * order) on `stream` (a cudaStream_t, the context's) and returns 0 -- e.g.
+ * pm_nccl_allgather_device.  The block records, the exchange and the
+ * generation step stay on the device: no host staging. */
+typedef int (*pm_allgather_device_fn)(const void* send_device, size_t bytes, void* recv_device, void* stream,
+                                      void* user);
+int pm_run_ga_islands_device(pm_ctx* ctx, const pm_ga_config* cfg, int rank, int world,
+                             pm_allgather_device_fn allgather, void* user, uint64_t* best_words,
+                             int64_t* per_kernel_best, pm_run_result* result);
+
+/* RunResult::per_kernel_best_costs of the last pm_run_ga* call on this
+ * context: *count = kernels executed; min(count, capacity) entries copied. */
+int pm_last_per_kernel_best(pm_ctx* ctx, int64_t* out, size_t capacity, size_t* count);
+
 /* Native island exchange over NCCL (NVLink/NVSwitch on one node) for C/C++
  * hosts without torch.distributed: one communicator per rank, created from a
  * unique id that rank 0 generates and the launcher distributes (file, MPI,
@@ -224,6 +251,11 @@ int pm_nccl_unique_id(char id[PM_NCCL_ID_BYTES]);
 int pm_nccl_create(const char id[PM_NCCL_ID_BYTES], int rank, int world, int device, pm_nccl** out);
 void pm_nccl_destroy(pm_nccl* comm);
 int pm_nccl_allgather(const void* send, size_t bytes, void* recv, void* user);
+/* pm_allgather_device_fn over the communicator: one ncclAllGather of device
+ * buffers enqueued on `stream` (asynchronous).  pass the pm_nccl* as `user`. */
+int pm_nccl_allgather_device(const void* send_device, size_t bytes, void* recv_device, void* stream, void* user);
+/* rank / world size of a communicator */
+int pm_nccl_rank(const pm_nccl* comm, int* rank, int* world);
 
 #ifdef __cplusplus
 }

@@ -148,24 +148,40 @@ class Tables {
   };
   RunResult run_ga(const pm_ga_config& cfg, int rank = 0, int world = 1, pm_allgather_fn allgather = nullptr,
                    void* user = nullptr) {
+    return run_ga_impl(cfg, rank, world, allgather, nullptr, user);
+  }
+  // Islands over a native NCCL communicator (pm_nccl_create / NcclIslands::comm()):
+  // the block records, their all-gather and the generation step stay on the GPU.
+  RunResult run_ga(const pm_ga_config& cfg, pm_nccl* comm) {
+    int rank = 0, world = 1;
+    check(pm_nccl_rank(comm, &rank, &world));
+    return run_ga_impl(cfg, rank, world, nullptr, pm_nccl_allgather_device, comm);
+  }
+
+ private:
+  RunResult run_ga_impl(const pm_ga_config& cfg, int rank, int world, pm_allgather_fn allgather,
+                        pm_allgather_device_fn dev, void* user) {
     const pm_table_info ti = info();
     RunResult r;
     r.best.assign((ti.sites + 63) / 64, 0);
-    r.per_kernel_best_costs.assign(cfg.evolve_limit, 0);
     pm_run_result res{};
-    check(world == 1 && !allgather
-              ? pm_run_ga(ctx_, &cfg, r.best.data(), r.per_kernel_best_costs.data(), &res)
-              : pm_run_ga_islands(ctx_, &cfg, rank, world, allgather, user, r.best.data(),
-                                  r.per_kernel_best_costs.data(), &res));
+    // per-kernel bests are read back afterwards: never a buffer sized by evolve_limit
+    check(dev ? pm_run_ga_islands_device(ctx_, &cfg, rank, world, dev, user, r.best.data(), nullptr, &res)
+              : world == 1 && !allgather
+              ? pm_run_ga(ctx_, &cfg, r.best.data(), nullptr, &res)
+              : pm_run_ga_islands(ctx_, &cfg, rank, world, allgather, user, r.best.data(), nullptr, &res));
     r.best_cost = res.best_cost;
     r.kernels_executed = res.kernels_executed;
     r.kernel_of_best = res.kernel_of_best;
     r.per_kernel_best_costs.resize(res.kernels_executed);
+    std::size_t cnt = 0;
+    check(pm_last_per_kernel_best(ctx_, r.per_kernel_best_costs.data(), r.per_kernel_best_costs.size(), &cnt));
     r.wall_time = res.wall_time_s;
     r.evaluations = res.evaluations;
     return r;
   }
 
+ public:
   std::vector<std::int64_t> min_cost_sum(const std::vector<std::uint64_t>& words, std::size_t count) const {
     std::vector<std::int64_t> out(count);
     if (count == 0) return out;

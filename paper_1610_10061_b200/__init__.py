@@ -48,6 +48,7 @@ _lib.pm_set_eval_kernel.argtypes = [_vp, C.c_int]
 _lib.pm_auto_eval_kernel.argtypes = [_vp]
 _lib.pm_min_cost_sum.argtypes = [_vp, _vp, _sz, _sz, _vp, C.POINTER(_sz)]
 _lib.pm_scan_depths_device.argtypes = [_vp, _vp, _sz, _sz, _vp]
+_lib.pm_scan_walks_device.argtypes = [_vp, _vp, _sz, _sz, _vp, _vp]
 _lib.pm_set_profiling.argtypes = [_vp, C.c_int]
 _lib.pm_profile_read.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
 
@@ -70,6 +71,10 @@ _lib.pm_evolve_blocks.argtypes = [_vp, _vp, _sz, _sz, C.POINTER(GaConfig), C.c_u
 _lib.pm_run_ga.argtypes = [_vp, C.POINTER(GaConfig), _vp, _vp, C.POINTER(_RunResult)]
 _lib.pm_run_ga_islands.argtypes = [_vp, C.POINTER(GaConfig), C.c_int, C.c_int, ALLGATHER_FN, _vp, _vp,
                                    _vp, C.POINTER(_RunResult)]
+ALLGATHER_DEVICE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p)
+_lib.pm_run_ga_islands_device.argtypes = [_vp, C.POINTER(GaConfig), C.c_int, C.c_int, _vp, _vp, _vp, _vp,
+                                          C.POINTER(_RunResult)]
+_lib.pm_last_per_kernel_best.argtypes = [_vp, _vp, _sz, C.POINTER(_sz)]
 _lib.pm_set_instance_orlib.argtypes = [_vp, C.c_char_p, _sz, _sz]
 _lib.pm_set_instance_dense.argtypes = [_vp, C.c_char_p, _sz, _sz]
 _lib.pm_orlib_closure.argtypes = [_vp, C.c_char_p, _sz, _vp, _sz, C.POINTER(_sz), C.POINTER(_sz)]
@@ -90,10 +95,11 @@ C_ABI_SYMBOLS = (
     "pm_create", "pm_destroy", "pm_last_error", "pm_set_stream", "pm_kernel_launches",
     "pm_set_instance", "pm_set_instance_device", "pm_table_info_get", "pm_get_tables",
     "pm_evaluate", "pm_evaluate_device", "pm_check_errors", "pm_set_eval_kernel",
-    "pm_auto_eval_kernel", "pm_min_cost_sum", "pm_scan_depths_device", "pm_set_profiling",
+    "pm_auto_eval_kernel", "pm_min_cost_sum", "pm_scan_depths_device", "pm_scan_walks_device", "pm_set_profiling",
     "pm_profile_read", "pm_evolve_blocks", "pm_run_ga", "pm_run_ga_islands", "pm_set_instance_orlib",
     "pm_orlib_closure", "pm_set_instance_dense", "pm_nccl_unique_id", "pm_nccl_create", "pm_nccl_destroy",
-    "pm_nccl_allgather",
+    "pm_nccl_allgather", "pm_nccl_allgather_device", "pm_nccl_rank", "pm_run_ga_islands_device",
+    "pm_last_per_kernel_best",
 )
 
 
@@ -112,6 +118,9 @@ _lib.pm_nccl_destroy.argtypes = [_vp]
 _lib.pm_nccl_destroy.restype = None
 _lib.pm_nccl_allgather.argtypes = [_vp, _sz, _vp, _vp]
 _NCCL_ALLGATHER = ALLGATHER_FN(("pm_nccl_allgather", _lib))
+# the device collective's address, passed straight back into the library (no Python in the loop)
+_NCCL_ALLGATHER_DEVICE = C.cast(_lib.pm_nccl_allgather_device, _vp)
+_lib.pm_nccl_rank.argtypes = [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
 NCCL_ID_BYTES = 128
 
 
@@ -395,6 +404,13 @@ class Context:
         self._after_torch(words)
         self._check(_lib.pm_scan_depths_device(self._h, _ptr(words), count, wp, _ptr(sum_k_out)))
 
+    def scan_walks_device(self, words, group_sum_out, client_max_out, count: int, wp: int) -> None:
+        """group_sum_out[g] (int64, ceil(count/32)) = sum_i max_{c in group g} k*_ic;
+        client_max_out[i] (int32, n) = max over groups (measurement only)."""
+        self._after_torch(words)
+        self._check(_lib.pm_scan_walks_device(self._h, _ptr(words), count, wp, _ptr(group_sum_out),
+                                              _ptr(client_max_out)))
+
     def set_profiling(self, on: bool) -> None:
         self._check(_lib.pm_set_profiling(self._h, int(on)))
 
@@ -419,21 +435,26 @@ class Context:
         return b, bc[:nb], bt[:nb].astype(np.int64)
 
     def run_ga(self, cfg: GaConfig, rank: int = 0, world: int = 1, allgather=None):
-        """pmedian::run_ga -> dict with the RunResult fields (ga.hpp:49-56) and work counters."""
+        """pmedian::run_ga -> dict with the RunResult fields (ga.hpp:49-56) and work counters.
+        allgather: None (one island), a NcclComm (the library's device NCCL exchange,
+        records never leave the GPU) or a pm_allgather_fn-shaped host callable."""
         wp = words_per(self.m)
         best = np.zeros(wp, dtype=np.uint64)
-        per = np.zeros(cfg.evolve_limit, dtype=np.int64)
         r = _RunResult()
         if world == 1 and allgather is None:
-            rc = _lib.pm_run_ga(self._h, C.byref(cfg), best.ctypes.data, per.ctypes.data, C.byref(r))
+            rc = _lib.pm_run_ga(self._h, C.byref(cfg), best.ctypes.data, None, C.byref(r))
         elif isinstance(allgather, NcclComm):  # the library's own NCCL exchange, no Python in the loop
-            rc = _lib.pm_run_ga_islands(self._h, C.byref(cfg), rank, world, _NCCL_ALLGATHER, allgather._h,
-                                        best.ctypes.data, per.ctypes.data, C.byref(r))
+            rc = _lib.pm_run_ga_islands_device(self._h, C.byref(cfg), rank, world, _NCCL_ALLGATHER_DEVICE,
+                                               allgather._h, best.ctypes.data, None, C.byref(r))
         else:
             cb = ALLGATHER_FN(allgather)
             rc = _lib.pm_run_ga_islands(self._h, C.byref(cfg), rank, world, cb, None, best.ctypes.data,
-                                        per.ctypes.data, C.byref(r))
+                                        None, C.byref(r))
         self._check(rc)
+        per = np.zeros(r.kernels_executed, dtype=np.int64)
+        cnt = _sz(0)
+        self._check(_lib.pm_last_per_kernel_best(self._h, per.ctypes.data if per.size else None, per.size,
+                                                 C.byref(cnt)))
         return dict(best=best, best_cost=r.best_cost, kernels_executed=r.kernels_executed,
                     kernel_of_best=r.kernel_of_best, per_kernel_best_costs=per[:r.kernels_executed].copy(),
                     wall_time=r.wall_time_s, evolve_time=r.evolve_time_s, evaluations=r.evaluations,

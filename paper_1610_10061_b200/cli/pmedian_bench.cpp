@@ -221,7 +221,6 @@ int main(int argc, char** argv) {
     std::vector<size_t> kernels;
     std::vector<double> times;
     std::vector<uint64_t> best((ti.sites + 63) / 64);
-    std::vector<int64_t> per(std::max<size_t>(1, cfg.evolve_limit));
     for (size_t r = 0; r < repeats; ++r) {
       pm_ga_config run = cfg;
       if (repeats > 1) {  // bench.cpp:249-252
@@ -230,7 +229,7 @@ int main(int argc, char** argv) {
         run.seed = s.next();
       }
       pm_run_result res{};
-      check(pm_run_ga(ctx, &run, best.data(), per.data(), &res));
+      check(pm_run_ga(ctx, &run, best.data(), nullptr, &res));
       costs.push_back(res.best_cost);
       kernels.push_back(res.kernel_of_best);
       times.push_back(res.wall_time_s);

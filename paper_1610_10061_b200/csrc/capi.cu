@@ -45,7 +45,8 @@ int pm_create(int device, pm_ctx** out) {
   if (c->errw.ensure(kErrSlots * 8) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->draw_stream, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->draw_ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->draw_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->entry_ev, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return PM_CUDA;
   }
@@ -62,10 +63,11 @@ void pm_destroy(pm_ctx* c) {
                     &c->costs_out, &c->T, &c->lists, &c->counts, &c->errw, &c->scal, &c->ga.pop,
                     &c->ga.next, &c->ga.cost, &c->ga.before, &c->ga.child, &c->ga.ccost, &c->ga.ok,
                     &c->ga.brec, &c->ga.evals, &c->ga.tmp, &c->ga.table, &c->ga.ranks, &c->ga.rflags,
-                    &c->ga.rstate})
+                    &c->ga.rstate, &c->ga.lfact, &c->ga.grec, &c->ga.gstate, &c->ga.perk, &c->sort_rows})
     b->release();
   c->ga.hrec.release();
-  c->ga.hmig.release();
+  c->ga.hglob.release();
+  c->ga.hflag.release();
   for (auto* v : {&c->ev_used, &c->ev_free})
     for (auto& e : *v) {
       cudaEventDestroy(e.first);
@@ -77,6 +79,7 @@ void pm_destroy(pm_ctx* c) {
     cudaStreamDestroy(c->draw_stream);
   }
   if (c->draw_ev) cudaEventDestroy(c->draw_ev);
+  if (c->entry_ev) cudaEventDestroy(c->entry_ev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
@@ -413,6 +416,12 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
   }
   unsigned long long* slots = c->errw.as<unsigned long long>() + 1;
   PM_CUDA_TRY(c, cudaMemsetAsync(slots, 0xff, chunks * 8, c->stream));
+  // the copies follow everything already queued on the compute stream (the
+  // call is ordered like one stream operation: a caller's event recorded
+  // before it brackets the whole transfer), and the scratch buffer `words` is
+  // free again once the previous call's kernels have read it
+  PM_CUDA_TRY(c, cudaEventRecord(c->entry_ev, c->stream));
+  PM_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->entry_ev, 0));
   int used = 0;
   for (size_t off = 0; off < count; off += per, ++used) {
     const size_t cnt = std::min(per, count - off);
@@ -447,6 +456,28 @@ int pm_scan_depths_device(pm_ctx* c, const uint64_t* bitsets_device, size_t coun
   if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
   size_t fb = 0;
   return evaluate_dev(c, bitsets_device, count, words_per, reinterpret_cast<int64_t*>(sum_k_device), &fb, 2);
+}
+
+int pm_scan_walks_device(pm_ctx* c, const uint64_t* bitsets_device, size_t count, size_t words_per,
+                         uint64_t* group_walk_sum_device, uint32_t* client_max_walk_device) {
+  if (!c) return PM_STRUCTURAL;
+  if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
+  if (words_per != (size_t)(c->t.m + 63) / 64) return c->fail(PM_STRUCTURAL, kMsgLength);
+  if (count == 0) return PM_OK;
+  PM_CUDA_TRY(c, cudaSetDevice(c->device));
+  const size_t groups = (count + 63) / 64;
+  PM_CUDA_TRY(c, c->T.ensure(groups * scan_t_stride(c->t.m) * 8));
+  PM_CUDA_TRY(c, c->scal.ensure(std::max<size_t>(16, count * 8)));
+  PM_CUDA_TRY(c, launch_transpose_population(bitsets_device, count, (int)words_per, c->t.m, c->T.as<uint64_t>(),
+                                             c->scal.as<unsigned long long>(), c->stream));
+  PM_CUDA_TRY(c, cudaMemsetAsync(group_walk_sum_device, 0, (count + 31) / 32 * 8, c->stream));
+  PM_CUDA_TRY(c, cudaMemsetAsync(client_max_walk_device, 0, (size_t)c->t.n * 4, c->stream));
+  PM_CUDA_TRY(c, launch_walks(c->t, c->T.as<uint64_t>(), count,
+                              reinterpret_cast<unsigned long long*>(group_walk_sum_device),
+                              client_max_walk_device, c->stream));
+  c->launches += 2;
+  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return PM_OK;
 }
 
 int pm_set_profiling(pm_ctx* c, int enabled) {

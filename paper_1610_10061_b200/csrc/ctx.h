@@ -80,7 +80,12 @@ struct GaBuffers {
   DevBuf pop, next, cost, before, child, ccost, ok, brec, evals, tmp, table, ranks, rflags, rstate;
   DevBuf lfact;  // ln x! for x <= m + 1 (double): the unranking's search guide
   size_t tab_m = 0, tab_p = 0, tab_L = 0;  // what `table` / `lfact` hold (0: nothing)
-  HostBuf hrec, hmig;
+  // run_ga's device-resident generation state: grec = every island's block
+  // records after the exchange, gstate = {best cost, kernel of best, stale,
+  // kernels, stop, best words[wp]}, perk = per-kernel bests (grown on demand)
+  DevBuf grec, gstate, perk;
+  size_t perk_cap = 0;
+  HostBuf hrec, hglob, hflag;  // pinned: host-callback exchange staging, the stop word
 };
 }  // namespace pmb
 using pmb::GaBuffers;
@@ -107,7 +112,9 @@ struct pm_ctx {
   cudaStream_t copy_stream = nullptr;  // H2D of pipelined host-buffer calls
   cudaStream_t draw_stream = nullptr;  // the GA's next-population draw, overlapped with evolution
   cudaEvent_t draw_ev = nullptr;
+  cudaEvent_t entry_ev = nullptr;  // host-buffer calls: copies start after the stream's earlier work
   std::vector<cudaEvent_t> chunk_ev;
+  std::vector<int64_t> per_kernel_best;  // RunResult::per_kernel_best_costs of the last run_ga
 
   // kernel timing hook: events around the dominant evaluation kernel
   bool profiling = false;

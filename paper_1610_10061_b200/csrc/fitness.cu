@@ -64,32 +64,36 @@ __global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __
                                                               unsigned long long* __restrict__ costs) {
   const int lane = threadIdx.x & 31;
   const int wi = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const size_t g = blockIdx.y;
-  uint64_t* Tg = T + g * Ts;
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    for (size_t s = (size_t)m + lane; s < Ts; s += 32) Tg[s] = 0;  // sentinel site m
+  const size_t groups = (count + 63) / 64;
+  // groups stride over gridDim.y (<= 65535) so any population size launches
+  for (size_t g = blockIdx.y; g < groups; g += gridDim.y) {
+    uint64_t* Tg = T + g * Ts;
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      for (size_t s = (size_t)m + lane; s < Ts; s += 32) Tg[s] = 0;  // sentinel site m
+    }
+    // the scan accumulates into costs: zero the group's 64 (replaces a memset launch)
+    if (blockIdx.x == 0 && threadIdx.x >= 64 && threadIdx.x < 128 && g * 64 + threadIdx.x - 64 < count)
+      costs[g * 64 + threadIdx.x - 64] = 0;
+    if (wi >= wp) continue;  // warp-uniform
+    const size_t c0 = g * 64 + lane, c1 = c0 + 32;
+    const uint64_t x = c0 < count ? words[c0 * wp + wi] : 0;
+    const uint64_t y = c1 < count ? words[c1 * wp + wi] : 0;
+    // four 32 x 32 bit transposes (butterfly over the lanes: 5 shuffle stages
+    // each): lane L ends with bit c = chromosome c opens site 64 wi + L (+ 32)
+    const uint64_t t0 =
+        (uint64_t)transpose32(lane, (uint32_t)x) | ((uint64_t)transpose32(lane, (uint32_t)y) << 32);
+    const uint64_t t1 = (uint64_t)transpose32(lane, (uint32_t)(x >> 32)) |
+                        ((uint64_t)transpose32(lane, (uint32_t)(y >> 32)) << 32);
+    const int s0 = wi * 64 + lane, s1 = s0 + 32;
+    if (s0 < m) Tg[s0] = t0;
+    if (s1 < m) Tg[s1] = t1;
   }
-  // the scan accumulates into costs: zero the group's 64 (replaces a memset launch)
-  if (blockIdx.x == 0 && threadIdx.x >= 64 && threadIdx.x < 128 && g * 64 + threadIdx.x - 64 < count)
-    costs[g * 64 + threadIdx.x - 64] = 0;
-  if (wi >= wp) return;  // warp-uniform
-  const size_t c0 = g * 64 + lane, c1 = c0 + 32;
-  const uint64_t x = c0 < count ? words[c0 * wp + wi] : 0;
-  const uint64_t y = c1 < count ? words[c1 * wp + wi] : 0;
-  // four 32 x 32 bit transposes (butterfly over the lanes: 5 shuffle stages
-  // each): lane L ends with bit c = chromosome c opens site 64 wi + L (+ 32)
-  const uint64_t t0 = (uint64_t)transpose32(lane, (uint32_t)x) | ((uint64_t)transpose32(lane, (uint32_t)y) << 32);
-  const uint64_t t1 =
-      (uint64_t)transpose32(lane, (uint32_t)(x >> 32)) | ((uint64_t)transpose32(lane, (uint32_t)(y >> 32)) << 32);
-  const int s0 = wi * 64 + lane, s1 = s0 + 32;
-  if (s0 < m) Tg[s0] = t0;
-  if (s1 < m) Tg[s1] = t1;
 }
 
 cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int words_per, int m,
                                         uint64_t* T, unsigned long long* costs, cudaStream_t st) {
   const size_t groups = (count + 63) / 64;
-  dim3 grid((words_per + 7) / 8, (unsigned)groups);
+  dim3 grid((words_per + 7) / 8, (unsigned)std::min<size_t>(groups, 65535));
   k_transpose_population<<<grid, 256, 0, st>>>(words, count, words_per, m, T, scan_t_stride(m), costs);
   return cudaGetLastError();
 }
@@ -574,6 +578,61 @@ cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* 
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// ---- measurement: per-(group, client) walk lengths ------------------------
+//
+// The scan's work per (32-chromosome group g, client i) is the row walk up to
+// the column where the last of the group's chromosomes finds an open site:
+// walk_gi = max_{c in g} k*_ic.  This kernel (measurement only -- never on the
+// evaluation path) reports sum_i walk_gi per group and max_g walk_gi per
+// client, from which bench.py derives the reuse-aware byte floors of the
+// roofline: the bytes K2 must stream from L2 (sum over groups) and the bytes
+// it must read from DRAM at least once (sum over clients of the maximum).
+// One thread per (group, client); masks read from the transposed population.
+template <class OrdT>
+__global__ void __launch_bounds__(256) k_walks(const OrdT* __restrict__ ord, int n, int W, int Wp,
+                                               const uint64_t* __restrict__ T, size_t Ts, size_t count,
+                                               unsigned long long* __restrict__ group_sum,
+                                               unsigned int* __restrict__ client_max) {
+  const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int groups = (int)((count + 31) / 32);
+  int walk = 0, g = 0;
+  if (u < (long long)groups * n) {
+    g = (int)(u / n);
+    const int i = (int)(u % n);
+    const uint64_t* Tg = T + (size_t)(g / 2) * Ts;
+    const int half = (g & 1) * 32;
+    const size_t nvalid = min((size_t)32, count - (size_t)g * 32);
+    uint32_t alive = nvalid == 32 ? ~0u : ((1u << nvalid) - 1);
+    const OrdT* row = ord + (size_t)i * Wp;
+    int k = 0;
+    for (; k < W && alive; ++k) alive &= ~(uint32_t)(__ldg(Tg + row[k]) >> half);
+    walk = k;
+    atomicMax(client_max + i, (unsigned)walk);
+  }
+  // lanes of a warp mostly share a group: one atomic per (warp, group) run
+  const int g0 = __shfl_sync(kFull, g, 0);
+  const bool same = __all_sync(kFull, g == g0 || u >= (long long)groups * n);
+  if (same) {
+    const unsigned long long s = warp_sum((unsigned long long)walk);
+    if (lane_id() == 0 && s) atomicAdd(group_sum + g0, s);
+  } else if (walk) {
+    atomicAdd(group_sum + g, (unsigned long long)walk);
+  }
+}
+
+cudaError_t launch_walks(const DevTables& t, const uint64_t* T, size_t count, unsigned long long* group_sum,
+                         unsigned int* client_max, cudaStream_t st) {
+  const long long units = (long long)((count + 31) / 32) * t.n;
+  const unsigned blocks = (unsigned)((units + 255) / 256);
+  if (t.site_bytes == 2)
+    k_walks<uint16_t><<<blocks, 256, 0, st>>>((const uint16_t*)t.ord, t.n, t.W, t.Wp, T, scan_t_stride(t.m),
+                                               count, group_sum, client_max);
+  else
+    k_walks<uint32_t><<<blocks, 256, 0, st>>>((const uint32_t*)t.ord, t.n, t.W, t.Wp, T, scan_t_stride(t.m),
+                                               count, group_sum, client_max);
+  return cudaGetLastError();
+}
+
 // ---- K2b: gather-min -----------------------------------------------------------
 
 // One warp per chromosome: compact the open sites (< m) into a list.
@@ -660,12 +719,12 @@ __global__ void __launch_bounds__(kGatherThreads)
   unsigned long long* part = reinterpret_cast<unsigned long long*>(smem);  // [warps][chunk]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kWarps = kGatherThreads / 32;
-  const size_t cbase = (size_t)blockIdx.y * chunk;
-  const int cn = (int)min((size_t)chunk, count - cbase);
   const int i0 = (blockIdx.x * kGatherThreads + tid) * V;  // first client of this thread
   const int nv = i0 < n ? min(V, n - i0) : 0;               // real clients among the V
   const DistT* col = dT + i0;
-
+  // chromosome chunks stride over gridDim.y (<= 65535): any population size launches
+  for (size_t cbase = (size_t)blockIdx.y * chunk; cbase < count; cbase += (size_t)gridDim.y * chunk) {
+  const int cn = (int)min((size_t)chunk, count - cbase);
   for (int cl = 0; cl < cn; ++cl) {
     const size_t c = cbase + cl;
     const uint32_t pc = counts[c];
@@ -738,6 +797,8 @@ __global__ void __launch_bounds__(kGatherThreads)
     for (int w = 0; w < kWarps; ++w) s += part[w * chunk + cl];
     atomicAdd(&costs[cbase + cl], s);
   }
+  __syncthreads();  // `part` is rewritten by the next chunk
+  }
 }
 
 template <class DistT, class OrdT>
@@ -750,7 +811,7 @@ static cudaError_t launch_gather_t(const DevTables& t, const uint64_t* words, si
   // enough CTAs for ~8 resident CTAs per SM
   const long long want = (long long)sms * 8;
   const int chunk = (int)std::max<long long>(1, std::min<long long>(256, (long long)count * xblocks / want));
-  const unsigned yblocks = (unsigned)((count + chunk - 1) / chunk);
+  const unsigned yblocks = (unsigned)std::min<size_t>((count + chunk - 1) / chunk, 65535);
   const size_t smem = (size_t)(kGatherThreads / 32) * chunk * 8;
   k_gather<DistT, OrdT><<<dim3(xblocks, yblocks), kGatherThreads, smem, st>>>(
       (const DistT*)t.dT, t.nP, (const OrdT*)t.ord, (const DistT*)t.dist, t.n, t.m, t.p, t.W, t.Wp, words,

@@ -234,6 +234,91 @@ __global__ void k_block_min(const int64_t* __restrict__ cost, const uint64_t* __
     rec[(size_t)b * (2 + wp) + 2 + w] = pop[((size_t)b * nt + t) * wp + w];
 }
 
+// run_ga's per-generation step (ga.cpp:279-297) on the device, after the
+// island exchange: every rank runs it on the same gathered records grec
+// (nb x {cost, thread, words[wp]}) and so reaches the same decision.
+//  * global best: strict <, lowest block wins ties (ga.cpp:279-282);
+//  * per-kernel best, best-so-far, kernel_of_best (1-based), stale counter,
+//    stop when stale >= saturation or kernel + 1 >= evolve_limit (:285-296);
+//  * migration only when continuing (:293-297) into the freshly drawn next
+//    population: block b's best to slot 0 of block b, or (team) every block's
+//    best to slots 0..nb-1 of block 0 (:204-215) -- local blocks only.
+// gstate: [0] best cost, [1] kernel_of_best, [2] stale, [3] kernels executed,
+// [4] stop, [5] reference-semantics evaluations at the stop, [8..8+wp) best words.
+constexpr int kStateWords = 8;
+__global__ void __launch_bounds__(256) k_generation_step(const uint64_t* __restrict__ grec, int nb, int wp,
+                                                         uint64_t kernel, uint64_t saturation, uint64_t limit,
+                                                         uint64_t* __restrict__ gstate, int64_t* __restrict__ perk,
+                                                         uint64_t* __restrict__ next, int nt, int team, int block0,
+                                                         int nbl, const unsigned long long* __restrict__ evals) {
+  __shared__ int64_t sc[8];
+  __shared__ int sb[8];
+  __shared__ int s_best, s_improved, s_stop;
+  const size_t rec = 2 + (size_t)wp;
+  int64_t best = INT64_MAX;
+  int bb = INT32_MAX;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const int64_t c = (int64_t)grec[(size_t)b * rec];
+    if (c < best || (c == best && b < bb)) {
+      best = c;
+      bb = b;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t c = __shfl_xor_sync(0xffffffffu, best, o);
+    const int b = __shfl_xor_sync(0xffffffffu, bb, o);
+    if (c < best || (c == best && b < bb)) {
+      best = c;
+      bb = b;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sc[warp] = best;
+    sb[warp] = bb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sc[w] < best || (sc[w] == best && sb[w] < bb)) {
+        best = sc[w];
+        bb = sb[w];
+      }
+    perk[kernel] = best;
+    const bool improved = best < (int64_t)gstate[0];
+    if (improved) {
+      gstate[0] = (uint64_t)best;
+      gstate[1] = kernel + 1;
+      gstate[2] = 0;
+    } else {
+      gstate[2] += 1;
+    }
+    const bool stop = gstate[2] >= saturation || kernel + 1 >= limit;
+    gstate[3] = kernel + 1;
+    gstate[4] = stop;
+    gstate[5] = *evals;
+    s_best = bb;
+    s_improved = improved;
+    s_stop = stop;
+  }
+  __syncthreads();
+  const int b = s_best;
+  if (s_improved)
+    for (int w = threadIdx.x; w < wp; w += blockDim.x) gstate[kStateWords + w] = grec[(size_t)b * rec + 2 + w];
+  if (s_stop) return;
+  if (!team) {
+    for (int x = threadIdx.x; x < nbl * wp; x += blockDim.x) {
+      const int lb = x / wp, w = x - lb * wp;
+      next[(size_t)lb * nt * wp + w] = grec[(size_t)(block0 + lb) * rec + 2 + w];
+    }
+  } else if (block0 == 0) {
+    for (int x = threadIdx.x; x < nb * wp; x += blockDim.x) {
+      const int gb = x / wp, w = x - gb * wp;
+      next[(size_t)gb * wp + w] = grec[(size_t)gb * rec + 2 + w];
+    }
+  }
+}
+
 // Device-native population draw: uniform p-subsets by Floyd's algorithm from a
 // keyed splitmix stream derive(seed, {4, generation, global chromosome}).
 // (Not the reference's BigInt unranking -- see population mode in pmedian_b200.h.)
@@ -780,6 +865,14 @@ static int validate_config(pm_ctx* c, const pm_ga_config* cfg) {
   return PM_OK;
 }
 
+// evolve_block's own checks only (ga.cpp:139-140): the run-level limits
+// (evolve_limit, saturation, team migration) belong to run_ga.
+static int validate_evolve_config(pm_ctx* c, const pm_ga_config* cfg) {
+  if (!cfg) return c->fail(PM_STRUCTURAL, "null config");
+  if (cfg->nt < 2 || (cfg->nt & (cfg->nt - 1)) != 0) return c->fail(PM_DOMAIN, "nt must be a power of two >= 2");
+  return PM_OK;
+}
+
 static GaShape make_shape(pm_ctx* c, const pm_ga_config* cfg, size_t nbl, size_t block0) {
   GaShape s;
   s.nbl = (int)nbl;
@@ -862,7 +955,7 @@ int pm_evolve_blocks(pm_ctx* c, uint64_t* blocks, size_t nb, size_t words_per, c
                      uint64_t kernel_index, size_t first_block, int64_t* best_cost, size_t* best_thread) {
   if (!c) return PM_STRUCTURAL;
   if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
-  int rc = validate_config(c, cfg);
+  int rc = validate_evolve_config(c, cfg);
   if (rc) return rc;
   if (words_per != (size_t)(c->t.m + 63) / 64) return c->fail(PM_STRUCTURAL, kMsgLength);
   if (nb == 0) return PM_OK;
@@ -904,13 +997,23 @@ int pm_evolve_blocks(pm_ctx* c, uint64_t* blocks, size_t nb, size_t words_per, c
   return PM_OK;
 }
 
-int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, pm_allgather_fn allgather,
-                      void* user, uint64_t* best_words, int64_t* per_kernel_best, pm_run_result* res) {
+}  // extern "C"
+
+namespace pmb {
+
+// run_ga over islands.  The block records never leave the device: k_block_min
+// writes them, the exchange (dev_fn: a device collective enqueued on the
+// context stream, e.g. NCCL; host_fn: a host callback through pinned staging)
+// gathers every island's records, and k_generation_step makes the global
+// decision and migrates on the device.  The host only reads the stop word.
+static int run_ga_impl(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, pm_allgather_fn host_fn,
+                       pm_allgather_device_fn dev_fn, void* user, uint64_t* best_words, int64_t* per_kernel_best,
+                       pm_run_result* res) {
   if (!c) return PM_STRUCTURAL;
   if (!c->has_instance) return c->fail(PM_CONTRACT, "no instance set");
   int rc = validate_config(c, cfg);
   if (rc) return rc;
-  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !allgather))
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !host_fn && !dev_fn))
     return c->fail(PM_DOMAIN, "invalid island layout");
   if (cfg->nb % (size_t)world != 0) return c->fail(PM_DOMAIN, "nb must be a multiple of the number of islands");
   PM_CUDA_TRY(c, cudaSetDevice(c->device));
@@ -1010,72 +1113,81 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
   PM_CUDA_TRY(c, cudaEventRecord(c->draw_ev, ds));
   PM_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->draw_ev, 0));
 
-  // per-block record exchanged between islands: {cost, thread, words[wp]},
-  // written by k_block_min and copied to pinned memory in one transfer
+  // per-block record exchanged between islands: {cost, thread, words[wp]}
   const size_t rec = 2 + wp;
-  PM_CUDA_TRY(c, B.hrec.ensure(nbl * rec * 8));
-  PM_CUDA_TRY(c, B.hmig.ensure(nb * wp * 8));
-  const uint64_t* local = B.hrec.as<uint64_t>();
-  uint64_t* mig = B.hmig.as<uint64_t>();
-  std::vector<uint64_t> global(nb * rec);
-  int64_t best_cost = std::numeric_limits<int64_t>::max();
-  std::vector<uint64_t> best(wp, 0);
-  size_t stale = 0, kernels = 0, kernel_of_best = 0;
+  const size_t bytes = nbl * rec * 8;
+  PM_CUDA_TRY(c, B.grec.ensure(nb * rec * 8));
+  PM_CUDA_TRY(c, B.gstate.ensure((kStateWords + wp) * 8));
+  PM_CUDA_TRY(c, B.hflag.ensure(64));
+  if (host_fn && world > 1) {
+    PM_CUDA_TRY(c, B.hrec.ensure(bytes));
+    PM_CUDA_TRY(c, B.hglob.ensure(nb * rec * 8));
+  }
+  {
+    std::vector<uint64_t> st(kStateWords + wp, 0);
+    st[0] = (uint64_t)std::numeric_limits<int64_t>::max();  // ga.cpp:241: kernel 0 always improves
+    PM_CUDA_TRY(c, cudaMemcpyAsync(B.gstate.p, st.data(), st.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // `st` is a host temporary
+  }
+  const uint64_t* grec = world > 1 ? B.grec.as<uint64_t>() : B.brec.as<uint64_t>();
+  uint64_t* flag = B.hflag.as<uint64_t>();
+  size_t kernels = 0;
   uint64_t device_evals = 0;
   double evolve_s = 0;
   const size_t kids_per_gen = count * (1 + (s.p >= 2 ? s.rounds : 0) + s.attempts);
   for (uint64_t kernel = 0;; ++kernel) {
     const auto g0 = std::chrono::steady_clock::now();
+    if (kernel >= B.perk_cap) {  // per-kernel bests: grown on demand, never sized by evolve_limit
+      const size_t cap = std::max<size_t>(64, 2 * B.perk_cap);
+      DevBuf grown;
+      PM_CUDA_TRY(c, grown.ensure(cap * 8));
+      if (kernel) PM_CUDA_TRY(c, cudaMemcpyAsync(grown.p, B.perk.p, kernel * 8, cudaMemcpyDeviceToDevice, c->stream));
+      PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      B.perk.release();
+      B.perk = grown;
+      grown.p = nullptr;
+      B.perk_cap = cap;
+    }
     rc = evolve_all(c, B, s, kernel);
     if (rc) return rc;
     device_evals += kids_per_gen;
     // draw the next population while the device evolves (ga.cpp:274)
     rc = draw(B.next, kernel + 1);
     if (rc) return rc;
-    PM_CUDA_TRY(c, cudaMemcpyAsync(B.hrec.p, B.brec.p, nbl * rec * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (world > 1 && dev_fn) {  // device collective on the context stream (NVLink / NVSwitch)
+      if (dev_fn(B.brec.p, bytes, B.grec.p, (void*)c->stream, user) != 0)
+        return c->fail(PM_NCCL, "island allgather failed");
+    } else if (world > 1) {  // host callback: pinned staging
+      PM_CUDA_TRY(c, cudaMemcpyAsync(B.hrec.p, B.brec.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+      PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      if (host_fn(B.hrec.p, bytes, B.hglob.p, user) != 0) return c->fail(PM_NCCL, "island allgather failed");
+      PM_CUDA_TRY(c, cudaMemcpyAsync(B.grec.p, B.hglob.p, nb * rec * 8, cudaMemcpyHostToDevice, c->stream));
+    }
+    // the step migrates into the next population: after its draw
+    PM_CUDA_TRY(c, cudaEventRecord(c->draw_ev, ds));
+    PM_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->draw_ev, 0));
+    k_generation_step<<<1, 256, 0, c->stream>>>(grec, (int)nb, (int)wp, kernel, cfg->saturation, cfg->evolve_limit,
+                                                B.gstate.as<uint64_t>(), B.perk.as<int64_t>(), B.next.as<uint64_t>(),
+                                                (int)nt, cfg->migration == PM_MIGRATE_TEAM, (int)block0, (int)nbl,
+                                                B.evals.as<unsigned long long>());
+    PM_CUDA_TRY(c, cudaGetLastError());
+    c->launches += 1;
+    PM_CUDA_TRY(c, cudaMemcpyAsync(flag, B.gstate.as<uint64_t>() + 4, 8, cudaMemcpyDeviceToHost, c->stream));
     PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     evolve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - g0).count();
-    if (world > 1) {
-      if (allgather(B.hrec.p, nbl * rec * 8, global.data(), user) != 0)
-        return c->fail(PM_NCCL, "island allgather failed");
-    } else {
-      std::memcpy(global.data(), local, nbl * rec * 8);
-    }
-    size_t best_block = 0;  // ga.cpp:279-282: strict <, lowest block wins ties
-    for (size_t b = 1; b < nb; ++b)
-      if ((int64_t)global[b * rec] < (int64_t)global[best_block * rec]) best_block = b;
-    const int64_t kernel_best = (int64_t)global[best_block * rec];
-    if (per_kernel_best && kernel < cfg->evolve_limit) per_kernel_best[kernel] = kernel_best;
-    if (kernel_best < best_cost) {  // ga.cpp:285-292
-      best_cost = kernel_best;
-      std::memcpy(best.data(), &global[best_block * rec + 2], wp * 8);
-      kernel_of_best = (size_t)kernel + 1;
-      stale = 0;
-    } else {
-      ++stale;
-    }
-    if (stale >= cfg->saturation || kernel + 1 >= cfg->evolve_limit) {
+    if (*flag) {
       kernels = (size_t)kernel + 1;
       break;
-    }
-    PM_CUDA_TRY(c, cudaEventRecord(c->draw_ev, ds));  // the next population is drawn
-    PM_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->draw_ev, 0));
-    // migrate (ga.cpp:204-215) into the freshly drawn population: one
-    // transfer from pinned staging (block b's best to slot 0 of block b, or
-    // in team mode every block's best to slots 0..nb-1 of block 0)
-    if (cfg->migration == PM_MIGRATE_BLOCK) {
-      for (size_t b = 0; b < nbl; ++b) std::memcpy(&mig[b * wp], &global[(block0 + b) * rec + 2], wp * 8);
-      PM_CUDA_TRY(c, cudaMemcpy2DAsync(B.next.p, nt * wp * 8, mig, wp * 8, wp * 8, nbl, cudaMemcpyHostToDevice,
-                                       c->stream));
-    } else if (rank == 0) {
-      for (size_t b = 0; b < nb; ++b) std::memcpy(&mig[b * wp], &global[b * rec + 2], wp * 8);
-      PM_CUDA_TRY(c, cudaMemcpyAsync(B.next.p, mig, nb * wp * 8, cudaMemcpyHostToDevice, c->stream));
     }
     std::swap(B.pop, B.next);
   }
   PM_CUDA_TRY(c, cudaStreamSynchronize(ds));  // the last (unused) draw
-  unsigned long long ref_evals = 0, rstate[3] = {0, 0, 0};
-  PM_CUDA_TRY(c, cudaMemcpyAsync(&ref_evals, B.evals.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<uint64_t> st(kStateWords + wp);
+  c->per_kernel_best.assign(kernels, 0);
+  unsigned long long rstate[3] = {0, 0, 0};
+  PM_CUDA_TRY(c, cudaMemcpyAsync(st.data(), B.gstate.p, st.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(c->per_kernel_best.data(), B.perk.p, kernels * 8, cudaMemcpyDeviceToHost,
+                                 c->stream));
   if (ref_draw && hd.L)
     PM_CUDA_TRY(c, cudaMemcpyAsync(rstate, B.rstate.p, 24, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1083,16 +1195,40 @@ int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, p
   size_t fb = 0;
   rc = pm_check_errors(c, &fb);
   if (rc) return rc;
-  if (best_words) std::memcpy(best_words, best.data(), wp * 8);
+  if (best_words) std::memcpy(best_words, &st[kStateWords], wp * 8);
+  if (per_kernel_best) std::memcpy(per_kernel_best, c->per_kernel_best.data(), kernels * 8);
   if (res) {
-    res->best_cost = best_cost;
+    res->best_cost = (int64_t)st[0];
     res->kernels_executed = kernels;
-    res->kernel_of_best = kernel_of_best;
+    res->kernel_of_best = (size_t)st[1];
     res->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     res->evolve_time_s = evolve_s;
-    res->evaluations = ref_evals + (uint64_t)kernels * count;  // + the initial evaluation of each generation
+    res->evaluations = st[5] + (uint64_t)kernels * count;  // + the initial evaluation of each generation
     res->device_evaluations = device_evals;
   }
+  return PM_OK;
+}
+
+}  // namespace pmb
+
+extern "C" {
+
+int pm_run_ga_islands(pm_ctx* c, const pm_ga_config* cfg, int rank, int world, pm_allgather_fn allgather,
+                      void* user, uint64_t* best_words, int64_t* per_kernel_best, pm_run_result* res) {
+  return pmb::run_ga_impl(c, cfg, rank, world, allgather, nullptr, user, best_words, per_kernel_best, res);
+}
+
+int pm_run_ga_islands_device(pm_ctx* c, const pm_ga_config* cfg, int rank, int world,
+                             pm_allgather_device_fn allgather, void* user, uint64_t* best_words,
+                             int64_t* per_kernel_best, pm_run_result* res) {
+  return pmb::run_ga_impl(c, cfg, rank, world, nullptr, allgather, user, best_words, per_kernel_best, res);
+}
+
+int pm_last_per_kernel_best(pm_ctx* c, int64_t* out, size_t capacity, size_t* count) {
+  if (!c) return PM_STRUCTURAL;
+  const size_t k = c->per_kernel_best.size();
+  if (count) *count = k;
+  if (out) std::memcpy(out, c->per_kernel_best.data(), std::min(k, capacity) * 8);
   return PM_OK;
 }
 

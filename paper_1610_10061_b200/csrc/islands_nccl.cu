@@ -118,4 +118,20 @@ int pm_nccl_allgather(const void* send, size_t bytes, void* recv, void* user) {
   return cudaStreamSynchronize(c->stream) == cudaSuccess ? PM_OK : PM_CUDA;
 }
 
+int pm_nccl_allgather_device(const void* send_device, size_t bytes, void* recv_device, void* stream, void* user) {
+  pm_nccl* c = static_cast<pm_nccl*>(user);
+  if (!c || (!send_device && bytes) || !recv_device) return PM_NCCL;
+  if (nccl().all_gather(send_device, recv_device, bytes, ncclUint8, c->comm, static_cast<cudaStream_t>(stream)) !=
+      ncclSuccess)
+    return PM_NCCL;
+  return PM_OK;
+}
+
+int pm_nccl_rank(const pm_nccl* c, int* rank, int* world) {
+  if (!c) return PM_STRUCTURAL;
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  return PM_OK;
+}
+
 }  // extern "C"

@@ -70,6 +70,13 @@ cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* 
                         unsigned long long* costs_acc, unsigned long long* err_first_bad,
                         int depth_mode, cudaStream_t st);
 
+// Measurement (not an evaluation path): per 32-chromosome group the sum over
+// clients of the walk length max_{c in group} k*_ic, and per client the
+// maximum over groups.  group_sum (ceil(count/32) u64) and client_max (n u32)
+// must be zeroed.  T from launch_transpose_population.
+cudaError_t launch_walks(const DevTables& t, const uint64_t* T, size_t count, unsigned long long* group_sum,
+                         unsigned int* client_max, cudaStream_t st);
+
 // K2b prep: per-chromosome open-site lists (cap entries) and popcounts.
 // also zeroes costs[0, count) (the gather accumulates into it)
 cudaError_t launch_open_lists(const uint64_t* words, size_t count, int words_per, int m,

@@ -192,6 +192,9 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 #pragma unroll
         for (int j = 0; j < 8; ++j) wh[(warp + 32 * j) * kHistPitch + lane] = 0;
         if (tid < 256) bucket[tid] += tcount[tid];
+        // the cells cleared above belong to other warps' columns, which those
+        // warps write again in the next tile: finish every clear first
+        __syncthreads();
       }
       __syncthreads();
       KeyT* tk = src;
@@ -289,6 +292,9 @@ __global__ void __launch_bounds__(kSortThreads, 1)
       A[x] = key;
       atomicAdd(&mycnt[(unsigned)(key >> sitebits) & dmask], 1u);
     }
+    // with no pass (every cost 0) the write-out below reads other warps'
+    // slices straight away: order it after every slice's keys (CTA-uniform)
+    if (npasses == 0) __syncthreads();
     KeyT* src = A;
     KeyT* dst = B;
     for (int q = 0; q < npasses; ++q) {

@@ -1,0 +1,172 @@
+"""Parity at the BASELINE sizes, table for table and chromosome for chromosome.
+
+The goldens come from the REFERENCE ITSELF (oracle/_ref = the unmodified
+/root/reference/proj/src, run by tests/golden/make_baseline_golden.py in the
+build container): SHA-256 digests of its build_ordering tables
+(ordering.cpp:10-38) in the exact byte layout pm_get_tables returns, its
+fitness() (ordering.cpp:40-59) of EVERY chromosome of each BASELINE batch on
+its own tables, and two of its run_ga RunResults (ga.cpp:219-303).  Here the
+device path is held to them:
+
+* K1 at pmed40 / syn5k / syn20k / sweep p = 10..1000: every table byte
+  (including the tie order of Pi', which fitness values cannot see);
+* K2 scan, K2b gather and AUTO on every chromosome of every batch
+  (pmed40-shape 15360, syn5k 1024, syn20k 4096, sweep 7 x 4096);
+* the paper's full Table-1 run at the pmed40 shape (evolve_limit 100,
+  saturation 10) and two generations of the syn20k island GA, 1 and 2 islands;
+* live, where oracle/_ref travelled with the snapshot: the reference's own
+  syn20k tables compared array for array with the device's.
+"""
+import hashlib
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(os.path.join(GOLDEN, "baseline_golden.json")) as f:
+        meta = json.load(f)
+    arrays = dict(np.load(os.path.join(GOLDEN, "baseline_golden.npz")))
+    return meta, arrays
+
+
+def _instance(ctx, npts, p):
+    import torch
+
+    from paper_1610_10061_b200 import synth
+    costs = synth.euclid_costs(npts, 12345, device="cuda")
+    ctx.set_instance(costs, npts, npts, p)
+    del costs
+    torch.cuda.empty_cache()
+
+
+def _check_tables(ctx, g, name):
+    so, inc = ctx.get_tables()
+    assert so.shape == (g["n"], g["width"]) and so.dtype == np.uint32 and inc.dtype == np.int64
+    for arr, key in ((so, "site_order"), (inc, "increments")):
+        if hashlib.sha256(arr.tobytes()).hexdigest() != g[f"{key}_sha256"]:
+            slab = g["slab_rows"]
+            bad = [r for r, want in zip(range(0, g["n"], slab), g[f"{key}_slabs"])
+                   if hashlib.sha256(arr[r:r + slab].tobytes()).hexdigest() != want]
+            pytest.fail(f"{name}: {key} differs from the reference build_ordering in row slabs {bad[:8]}")
+
+
+SHAPES = ["pmed40", "syn5k", "syn20k", "sweep10", "sweep20", "sweep50", "sweep100", "sweep200", "sweep500",
+          "sweep1000"]
+
+
+@pytest.mark.parametrize("name", SHAPES)
+def test_tables_and_every_chromosome_match_reference(ctx, pm, oracle, golden, name):
+    meta, arrays = golden
+    g = meta["shapes"][name]
+    _instance(ctx, g["n"], g["p"])
+    _check_tables(ctx, g, name)
+    pop = oracle.random_population(g["m"], g["p"], g["count"], seed=g["population_seed"])
+    want = arrays[f"{name}/fitness"]
+    assert int(want.sum()) == g["fitness_sum"]
+    for kind in (pm.EVAL_AUTO, pm.EVAL_SCAN, pm.EVAL_GATHER):
+        ctx.set_eval_kernel(kind)
+        got = ctx.evaluate(pop)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, f"{name} kernel {kind}: {bad.size} chromosomes differ, first {bad[:5]}"
+    ctx.set_eval_kernel(pm.EVAL_AUTO)
+
+
+def _runresult(r):
+    return dict(best_cost=int(r["best_cost"]), kernels_executed=int(r["kernels_executed"]),
+                kernel_of_best=int(r["kernel_of_best"]),
+                per_kernel_best_costs=[int(x) for x in r["per_kernel_best_costs"]],
+                best_words=[int(x) for x in r["best"]])
+
+
+def _want(gr):
+    return {k: gr[k] for k in ("best_cost", "kernels_executed", "kernel_of_best", "per_kernel_best_costs",
+                               "best_words")}
+
+
+def test_table1_full_run_matches_reference_run_ga(ctx, pm, golden):
+    """The paper's Table-1 settings (nb=60, nt=256, evolve_limit=100,
+    saturation=10, seed 1; acceptance.cpp:323-328) at the pmed40 shape: the
+    whole run, every generation's best, equals the reference run_ga."""
+    gr = golden[0]["ga"]["table1_pmed40_shape"]
+    _instance(ctx, gr["n"], gr["p"])
+    cfg = pm.ga_config(nb=gr["nb"], nt=gr["nt"], evolve_limit=gr["evolve_limit"], saturation=gr["saturation"],
+                       seed=gr["seed"])
+    assert _runresult(ctx.run_ga(cfg)) == _want(gr)
+
+
+def test_syn20k_island_ga_matches_reference_run_ga(ctx, pm, golden):
+    gr = golden[0]["ga"]["syn20k_islands_2gen"]
+    _instance(ctx, gr["n"], gr["p"])
+    cfg = pm.ga_config(nb=gr["nb"], nt=gr["nt"], evolve_limit=gr["evolve_limit"], saturation=gr["saturation"],
+                       seed=gr["seed"])
+    assert _runresult(ctx.run_ga(cfg)) == _want(gr)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _island_rank(rank, world, port, gr, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1610_10061_b200 as pm
+    ctx = pm.Context(0)
+    _instance(ctx, gr["n"], gr["p"])
+    cfg = pm.ga_config(nb=gr["nb"], nt=gr["nt"], evolve_limit=gr["evolve_limit"], saturation=gr["saturation"],
+                       seed=gr["seed"])
+    r = ctx.run_ga(cfg, rank=rank, world=world, allgather=pm.torch_allgather())
+    q.put((rank, _runresult(r)))
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_syn20k_island_ga_two_islands_matches_reference(golden):
+    """BASELINE config 4's split: the 16 blocks as 2 islands of 8 (two ranks on
+    one GPU, host gloo exchange -- no kernel waits on another rank) give the
+    reference run_ga's RunResult."""
+    import torch.multiprocessing as mp
+    gr = golden[0]["ga"]["syn20k_islands_2gen"]
+    c = mp.get_context("spawn")
+    q = c.Queue()
+    port = _free_port()
+    procs = [c.Process(target=_island_rank, args=(r, 2, port, gr, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join(60)
+    for rank, out in res:
+        assert out == _want(gr), rank
+
+
+def test_syn20k_tables_live_against_reference_build_ordering(ctx, pm, oracle, reflib):
+    """The reference's own build_ordering run now (single-threaded, ~30-100 s
+    at 20000 x 20000), compared array for array with the device tables, and its
+    fitness() on its own tables for every syn20k chromosome."""
+    n, p = 20000, 200
+    costs = oracle.synth_euclid(n)
+    ri = reflib.create(n, n, p, costs)
+    assert ri.rc == 0
+    _instance(ctx, n, p)
+    so, inc = ctx.get_tables()
+    rso, rinc = ri.tables()
+    assert np.array_equal(so, rso) and np.array_equal(inc, rinc)
+    del so, inc, rso, rinc
+    pop = oracle.random_population(n, p, 4096, seed=7)
+    rc, want, _ = ri.evaluate(pop, len(os.sched_getaffinity(0)))
+    assert rc == 0
+    assert np.array_equal(ctx.evaluate(pop), want)

@@ -5,10 +5,14 @@ test_instance.cpp) plus tests/golden/ref_vectors.npz produced by the reference
 itself (tests/golden/make_golden.py).  When oracle/_ref is built, the oracle is
 also compared with the live reference on fresh random instances.
 """
+import os
+
 import numpy as np
 import pytest
 
 from oracle.oracle import bits_to_words, open_to_words, words_per
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def test_example1_tables(oracle, example1):  # test_formulation.cpp:18-39
@@ -139,3 +143,22 @@ def test_synthetic_generators_deterministic(oracle):
     assert (pa == oracle.random_population(100, 7, 10)).all()
     pcs = [sum(bin(int(x)).count("1") for x in row) for row in pa]
     assert pcs == [7] * 10
+
+
+@pytest.mark.parametrize("name", ["pmed40", "syn5k"])
+def test_oracle_matches_reference_baseline_golden(oracle, name):
+    """The C restatement against the reference's own outputs at BASELINE shapes
+    (tests/golden/baseline_golden.*, made by the reference): every table byte
+    (SHA-256 of the pm_get_tables layout) and every chromosome's fitness."""
+    import hashlib
+    import json
+    meta = json.load(open(os.path.join(GOLDEN, "baseline_golden.json")))["shapes"][name]
+    want = np.load(os.path.join(GOLDEN, "baseline_golden.npz"))[f"{name}/fitness"]
+    n, p = meta["n"], meta["p"]
+    costs = oracle.synth_euclid(n)
+    so, inc = oracle.build_ordering(n, n, p, costs)
+    assert hashlib.sha256(so.tobytes()).hexdigest() == meta["site_order_sha256"]
+    assert hashlib.sha256(inc.tobytes()).hexdigest() == meta["increments_sha256"]
+    pop = oracle.random_population(n, p, meta["count"], seed=meta["population_seed"])
+    rc, got, _, _ = oracle.evaluate(so, inc, n, pop)
+    assert rc == 0 and (got == want).all()
