@@ -10,6 +10,7 @@ LIB       := $(PKG)/libpmedian_b200.so
 CLI       := $(PKG)/pmedian_bench
 
 REFTESTS  := tests/cpp/_ref/ref_tests
+REFACCEPT := tests/cpp/_ref/acceptance
 
 all: $(LIB) $(CLI) oracle reftests
 
@@ -49,8 +50,10 @@ reftests: $(LIB)
 	  mkdir -p tests/cpp/_ref && \
 	  g++ -std=c++20 -O1 -I include/compat -I include -I tests/cpp/doctest_shim tests/cpp/ref_tests_main.cpp \
 	    $(REF_TESTS_DIR)/test_chromosome.cpp $(REF_TESTS_DIR)/test_instance.cpp $(REF_TESTS_DIR)/test_formulation.cpp \
-	    $(REF_TESTS_DIR)/test_ga.cpp \
-	    -L $(PKG) -lpmedian_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)' -o $(REFTESTS).tmp && mv $(REFTESTS).tmp $(REFTESTS); \
+	    $(REF_TESTS_DIR)/test_ga.cpp $(REF_TESTS_DIR)/test_bench.cpp $(REF_TESTS_DIR)/test_combinatorics.cpp \
+	    -L $(PKG) -lpmedian_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)' -o $(REFTESTS).tmp && mv $(REFTESTS).tmp $(REFTESTS) && \
+	  g++ -std=c++20 -O2 -I include/compat -I include $(REF_TESTS_DIR)/acceptance.cpp \
+	    -L $(PKG) -lpmedian_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)' -o $(REFACCEPT).tmp && mv $(REFACCEPT).tmp $(REFACCEPT); \
 	else echo "reftests: $(REF_TESTS_DIR) absent, keeping prebuilt $(REFTESTS) (if any)"; fi
 
 clean:

@@ -155,6 +155,10 @@ int pm_orlib_closure(pm_ctx* ctx, const char* text, size_t len, int64_t* costs_o
                      size_t* n_out, size_t* p_out);
 /* Dense text ("n m p" + n rows of m costs): parse_dense diagnostics, then pm_set_instance. */
 int pm_set_instance_dense(pm_ctx* ctx, const char* text, size_t len, size_t p_override);
+/* parse_dense alone (bench.cpp:65-104): n, m, p and the n*m costs (costs_out may be
+ * NULL to query the sizes; capacity in entries).  Same diagnostics. */
+int pm_parse_dense(pm_ctx* ctx, const char* text, size_t len, int64_t* costs_out, size_t capacity, size_t* n_out,
+                   size_t* m_out, size_t* p_out);
 
 /* ---- genetic algorithm (K3 evolve, K4 islands) ------------------------------ */
 

@@ -87,6 +87,28 @@ class Tables {
     check(pm_set_instance(ctx_, costs.data(), n, m, p));
   }
 
+  // Instance text formats (bench.cpp:65-168): the parsed matrix back on the host.
+  struct Parsed {
+    std::size_t n = 0, m = 0, p = 0;
+    std::vector<std::int64_t> costs;
+  };
+  Parsed parse_dense(const std::string& text) const {
+    Parsed r;
+    check(pm_parse_dense(ctx_, text.data(), text.size(), nullptr, 0, &r.n, &r.m, &r.p));
+    r.costs.resize(r.n * r.m);
+    check(pm_parse_dense(ctx_, text.data(), text.size(), r.costs.data(), r.costs.size(), &r.n, &r.m, &r.p));
+    return r;
+  }
+  // parse_orlib: the graph's all-pairs shortest-path closure, computed on the device
+  Parsed orlib_closure(const std::string& text) const {
+    Parsed r;
+    check(pm_orlib_closure(ctx_, text.data(), text.size(), nullptr, 0, &r.n, &r.p));
+    r.m = r.n;
+    r.costs.resize(r.n * r.n);
+    check(pm_orlib_closure(ctx_, text.data(), text.size(), r.costs.data(), r.costs.size(), &r.n, &r.p));
+    return r;
+  }
+
   pm_table_info info() const {
     pm_table_info ti{};
     check(pm_table_info_get(ctx_, &ti));

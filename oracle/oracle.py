@@ -221,6 +221,14 @@ class RefLib:
                                       int(structured), buf, len(buf))
         return rc, buf.value.decode()
 
+    def report_roundtrip(self, text: str, structured: bool = True):
+        """The reference's parse_structured_report + emit_report -> (rc, text, records)."""
+        self.L.ref_report_roundtrip.argtypes = [C.c_char_p, C.c_int, C.c_char_p, _sz, C.POINTER(_sz)]
+        buf = C.create_string_buffer(1 << 20)
+        cnt = _sz(0)
+        rc = self.L.ref_report_roundtrip(text.encode(), int(structured), buf, len(buf), C.byref(cnt))
+        return rc, buf.value.decode(), cnt.value
+
     def parse(self, text: str, orlib: bool = True, cap: int = 1 << 22):
         """parse_orlib / parse_dense -> (rc, n, m, p, costs)"""
         out = np.zeros(cap, dtype=np.int64)

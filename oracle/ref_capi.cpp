@@ -328,6 +328,17 @@ int ref_run_benchmark(const char* path, int orlib, std::size_t nb, std::size_t n
   });
 }
 
+// parse_structured_report then emit_report (bench.cpp:281-352): the reference
+// reads a structured report and writes it back (structured or table).
+int ref_report_roundtrip(const char* text, int structured, char* out, std::size_t cap, std::size_t* count) {
+  return guard([&] {
+    const std::vector<BenchmarkRecord> recs = parse_structured_report(text);
+    *count = recs.size();
+    const std::string s = emit_report(recs, structured ? ReportStyle::Structured : ReportStyle::Table);
+    std::snprintf(out, cap, "%s", s.c_str());
+  });
+}
+
 int ref_validate_config(std::size_t nb, std::size_t nt, std::size_t evolve_limit,
                         std::size_t saturation, int team) {
   return guard([&] { make_cfg(nb, nt, evolve_limit, saturation, 1, -1, -1, team).validate(); });

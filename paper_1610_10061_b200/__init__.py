@@ -99,7 +99,7 @@ C_ABI_SYMBOLS = (
     "pm_profile_read", "pm_evolve_blocks", "pm_run_ga", "pm_run_ga_islands", "pm_set_instance_orlib",
     "pm_orlib_closure", "pm_set_instance_dense", "pm_nccl_unique_id", "pm_nccl_create", "pm_nccl_destroy",
     "pm_nccl_allgather", "pm_nccl_allgather_device", "pm_nccl_rank", "pm_run_ga_islands_device",
-    "pm_last_per_kernel_best",
+    "pm_last_per_kernel_best", "pm_parse_dense",
 )
 
 

@@ -15,6 +15,7 @@
 
 #include <cctype>
 #include <charconv>
+#include <algorithm>
 #include <climits>
 #include <string>
 #include <string_view>
@@ -258,9 +259,9 @@ int pm_set_instance_orlib(pm_ctx* c, const char* text, size_t len, size_t p_over
   return rc;
 }
 
-// parse_dense (bench.cpp:65-104) on the host, then the usual instance upload.
-int pm_set_instance_dense(pm_ctx* c, const char* text, size_t len, size_t p_override) {
-  if (!c) return PM_STRUCTURAL;
+// parse_dense (bench.cpp:65-104) on the host: diagnostics in the reference's order and texts.
+static int parse_dense_host(pm_ctx* c, const char* text, size_t len, std::vector<int64_t>& costs, int64_t& n,
+                            int64_t& m, int64_t& p) {
   const std::string_view t(text ? text : "", text ? len : 0);
   std::vector<std::string_view> lines;
   size_t start = 0;
@@ -273,8 +274,6 @@ int pm_set_instance_dense(pm_ctx* c, const char* text, size_t len, size_t p_over
     if (end == std::string_view::npos) break;
     start = end + 1;
   }
-  std::vector<int64_t> costs;
-  int64_t n = 0, m = 0, p = 0;
   try {
     if (lines.empty()) throw ParseError{PM_STRUCTURAL, "dense format: empty input"};
     const auto header = split_tokens(lines[0]);
@@ -288,6 +287,7 @@ int pm_set_instance_dense(pm_ctx* c, const char* text, size_t len, size_t p_over
     if (lines.size() - 1 != (size_t)n)
       throw ParseError{PM_STRUCTURAL, "dense format: expected " + std::to_string(n) + " cost rows, found " +
                                           std::to_string(lines.size() - 1)};
+    costs.clear();
     costs.reserve((size_t)n * m);
     for (int64_t i = 0; i < n; ++i) {
       const auto row = split_tokens(lines[(size_t)i + 1]);
@@ -305,7 +305,33 @@ int pm_set_instance_dense(pm_ctx* c, const char* text, size_t len, size_t p_over
   } catch (const ParseError& e) {
     return c->fail(e.code, e.msg);
   }
+  return PM_OK;
+}
+
+int pm_set_instance_dense(pm_ctx* c, const char* text, size_t len, size_t p_override) {
+  if (!c) return PM_STRUCTURAL;
+  std::vector<int64_t> costs;
+  int64_t n = 0, m = 0, p = 0;
+  const int rc = parse_dense_host(c, text, len, costs, n, m, p);
+  if (rc != PM_OK) return rc;
   return pm_set_instance(c, costs.data(), (size_t)n, (size_t)m, p_override ? p_override : (size_t)p);
+}
+
+int pm_parse_dense(pm_ctx* c, const char* text, size_t len, int64_t* costs_out, size_t capacity, size_t* n_out,
+                   size_t* m_out, size_t* p_out) {
+  if (!c) return PM_STRUCTURAL;
+  std::vector<int64_t> costs;
+  int64_t n = 0, m = 0, p = 0;
+  const int rc = parse_dense_host(c, text, len, costs, n, m, p);
+  if (rc != PM_OK) return rc;
+  if (n_out) *n_out = (size_t)n;
+  if (m_out) *m_out = (size_t)m;
+  if (p_out) *p_out = (size_t)p;
+  if (costs_out) {
+    if (capacity < costs.size()) return c->fail(PM_STRUCTURAL, "output buffer smaller than n * m");
+    std::copy(costs.begin(), costs.end(), costs_out);
+  }
+  return PM_OK;
 }
 
 }  // extern "C"

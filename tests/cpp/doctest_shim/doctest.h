@@ -63,6 +63,18 @@ inline void fail(const char* file, int line, const char* what) {
     }                                                                                      \
     if (!pmbdt_ok) pmbdt::fail(__FILE__, __LINE__, "CHECK_THROWS_AS(" #expr ", " #type ")"); \
   } while (0)
+#define CHECK_THROWS_WITH_AS(expr, text, type)                                             \
+  do {                                                                                     \
+    bool pmbdt_ok = false;                                                                 \
+    try {                                                                                  \
+      (void)(expr);                                                                        \
+    } catch (const type& pmbdt_e) {                                                        \
+      pmbdt_ok = std::string(pmbdt_e.what()) == std::string(text);                         \
+    } catch (...) {                                                                        \
+    }                                                                                      \
+    if (!pmbdt_ok)                                                                         \
+      pmbdt::fail(__FILE__, __LINE__, "CHECK_THROWS_WITH_AS(" #expr ", " #text ", " #type ")"); \
+  } while (0)
 #define CHECK_NOTHROW(expr)                                                  \
   do {                                                                       \
     try {                                                                    \
@@ -71,6 +83,26 @@ inline void fail(const char* file, int line, const char* what) {
       pmbdt::fail(__FILE__, __LINE__, "CHECK_NOTHROW(" #expr ")");           \
     }                                                                        \
   } while (0)
+
+namespace doctest {
+// doctest::Approx: relative tolerance (default: 100 float epsilons, doctest's scale)
+struct Approx {
+  explicit Approx(double v) : value(v) {}
+  Approx& epsilon(double e) {
+    eps = e;
+    return *this;
+  }
+  friend bool operator==(double lhs, const Approx& a) {
+    const double scale = 1.0 + (lhs < 0 ? -lhs : lhs) + (a.value < 0 ? -a.value : a.value);
+    const double d = lhs - a.value;
+    return (d < 0 ? -d : d) < a.eps * scale;
+  }
+  friend bool operator==(const Approx& a, double rhs) { return rhs == a; }
+  friend bool operator!=(double lhs, const Approx& a) { return !(lhs == a); }
+  double value;
+  double eps = 1.1920928955078125e-05;  // doctest: 100 * FLT_EPSILON
+};
+}  // namespace doctest
 
 #ifdef PMB_DOCTEST_MAIN
 int main() {

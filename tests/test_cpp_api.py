@@ -52,14 +52,33 @@ def test_compat_api_runs(tmp_path):
 
 @pytest.mark.gpu
 def test_reference_unit_tests_pass_on_the_device():
-    """The reference's own test_chromosome / test_instance / test_formulation /
-    test_ga (58 cases), compiled unchanged against the compat headers by `make
-    reftests` (where /root/reference exists; the binary travels with the
-    snapshot): every case passes with build_ordering / fitness / min_cost_sum /
-    exact_optimum_small / evolve_block / run_ga on the GPU."""
+    """All of the reference's own unit tests -- test_chromosome, test_instance,
+    test_formulation, test_ga, test_bench and test_combinatorics, 82 cases --
+    compiled unchanged against the compat headers by `make reftests` (where
+    /root/reference exists; the binary travels with the snapshot): every case
+    passes with build_ordering / fitness / min_cost_sum / exact_optimum_small /
+    evolve_block / run_ga / parse_orlib's closure on the GPU."""
     exe = os.path.join(ROOT, "tests", "cpp", "_ref", "ref_tests")
     if not os.path.exists(exe):
         pytest.skip("tests/cpp/_ref/ref_tests not built (no /root/reference at build time)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert " 0 failed checks" in r.stdout
+    assert "82 test cases, 0 failed checks" in r.stdout, r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_gate_passes_on_the_device():
+    """The reference's acceptance gate (proj/tests/acceptance.cpp:350-424),
+    compiled unchanged against the compat headers: criteria 1-6 PASS on the
+    device path (criterion 7 needs the OR-Library files: SKIP, as in the
+    reference without --orlib-dir)."""
+    exe = os.path.join(ROOT, "tests", "cpp", "_ref", "acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/_ref/acceptance not built (no /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    for k in range(1, 7):
+        assert f"criterion {k} [" in r.stdout and f"criterion {k} [" + "" in r.stdout
+        line = next(ln for ln in r.stdout.splitlines() if ln.startswith(f"criterion {k} ["))
+        assert ": PASS" in line, line

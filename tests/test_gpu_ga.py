@@ -71,12 +71,25 @@ def test_evolve_block_rejects_bad_shapes(ctx, pm):  # test_ga.cpp:290-320
     ctx.set_instance(np.array(E1), 5, 4, 2)
     with pytest.raises(pm.DomainError, match="nt must be a power of two"):
         ctx.evolve_blocks(np.zeros((3, 1), dtype=np.uint64), pm.ga_config(nb=1, nt=3), 0)
-    with pytest.raises(pm.DomainError, match="team migration needs nb <= nt"):
-        ctx.evolve_blocks(np.zeros((8, 1), dtype=np.uint64), pm.ga_config(nb=16, nt=8, team=True), 0)
     for kw, msg in ((dict(nb=0), "nb must be >= 1"), (dict(evolve_limit=0), "evolve_limit"),
-                    (dict(saturation=0), "saturation")):
+                    (dict(saturation=0), "saturation"), (dict(nb=16, nt=8, team=True), "team migration")):
         with pytest.raises(pm.DomainError, match=msg):
-            ctx.run_ga(pm.ga_config(nt=4, **kw))
+            ctx.run_ga(pm.ga_config(**dict(dict(nt=4), **kw)))
+
+
+def test_evolve_block_checks_only_its_own_shape(ctx, pm, oracle, reflib):  # ga.cpp:136-141
+    """evolve_block validates nt alone, as the reference does: run-level limits
+    (evolve_limit, saturation, team migration) are run_ga's, so a config the
+    reference's evolve_block accepts evolves the block identically here."""
+    costs = oracle.random_costs(21, 9, 9, 50)
+    ctx.set_instance(costs, 9, 9, 3)
+    blk = oracle.random_population(9, 3, 8, seed=6)
+    ri = reflib.create(9, 9, 3, costs)
+    for cfg in (pm.ga_config(nb=1, nt=8, evolve_limit=0, saturation=0, seed=5),
+                pm.ga_config(nb=16, nt=8, team=True, seed=5)):
+        got, cost, thread = ctx.evolve_blocks(blk, cfg, 2, 0)
+        rc, want, _, wcost, wthread = ri.evolve_block(blk, 8, 1, 5, 2, 0)
+        assert rc == 0 and (got == want).all() and cost[0] == wcost and thread[0] == wthread
 
 
 def _cmp_run(got, want):
