@@ -14,6 +14,7 @@
 #include <limits>
 #include <memory>
 #include <mutex>
+#include <utility>
 #include <span>
 #include <vector>
 
@@ -24,16 +25,69 @@
 namespace pmedian {
 
 namespace detail {
-// One device context holding the instance's resident tables.
-struct Device {
-  std::mutex mu;
-  b200::Tables tables;
-  explicit Device(int device) : tables(device) {}
-};
 inline int default_device() {
   const char* d = std::getenv("PMEDIAN_B200_DEVICE");
   return d ? std::atoi(d) : 0;
 }
+
+// Device contexts are reused across Instances: a context keeps its streams and
+// grow-only device buffers, so building the next instance costs the kernels
+// and copies alone (the reference builds small instances in microseconds,
+// acceptance.cpp:52-81).  The pool lives for the whole process.
+class ContextPool {
+ public:
+  static ContextPool& get() {
+    static ContextPool* p = new ContextPool;  // never destroyed: Instances may outlive static destruction
+    return *p;
+  }
+  std::unique_ptr<b200::Tables> take(int device) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      for (auto it = free_.begin(); it != free_.end(); ++it)
+        if (it->first == device) {
+          auto t = std::move(it->second);
+          free_.erase(it);
+          return t;
+        }
+    }
+    return std::make_unique<b200::Tables>(device);
+  }
+  void give(int device, std::unique_ptr<b200::Tables> t) {
+    std::lock_guard<std::mutex> lock(mu_);
+    if (free_.size() < 8) free_.emplace_back(device, std::move(t));
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<int, std::unique_ptr<b200::Tables>>> free_;
+};
+
+// One device context holding the instance's resident tables.
+struct Device {
+  std::mutex mu;
+  int device;
+  std::unique_ptr<b200::Tables> owned;
+  b200::Tables& tables;
+  explicit Device(int dev) : device(dev), owned(ContextPool::get().take(dev)), tables(*owned) {}
+  ~Device() { ContextPool::get().give(device, std::move(owned)); }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+};
+
+// CUDA context creation is a one-time process cost (hundreds of ms); it is
+// paid at program start, with one pooled context ready, not inside the first
+// Instance a caller times.  No-op without a device.
+inline bool warm_device() {
+  const int dev = default_device();
+  if (pm_warmup(dev) != PM_OK) return false;
+  try {
+    ContextPool::get().give(dev, ContextPool::get().take(dev));
+  } catch (...) {
+    return false;
+  }
+  return true;
+}
+inline const bool kDeviceWarm = warm_device();
 }  // namespace detail
 
 class Instance {

@@ -63,6 +63,9 @@ typedef struct pm_table_info {
 
 /* ---- context ----------------------------------------------------------- */
 
+/* Initialises the CUDA runtime on `device` (the one-time context creation,
+ * hundreds of milliseconds) without creating a pm_ctx; PM_CUDA without a device. */
+int pm_warmup(int device);
 /* Creates a context on CUDA device `device` with its own non-blocking stream. */
 int pm_create(int device, pm_ctx** out);
 void pm_destroy(pm_ctx* ctx);

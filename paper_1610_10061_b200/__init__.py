@@ -92,7 +92,7 @@ _lib.pm_table_info_get.argtypes = [_vp, C.POINTER(_TableInfo)]
 
 EVAL_AUTO, EVAL_SCAN, EVAL_GATHER = 0, 1, 2
 C_ABI_SYMBOLS = (
-    "pm_create", "pm_destroy", "pm_last_error", "pm_set_stream", "pm_kernel_launches",
+    "pm_warmup", "pm_create", "pm_destroy", "pm_last_error", "pm_set_stream", "pm_kernel_launches",
     "pm_set_instance", "pm_set_instance_device", "pm_table_info_get", "pm_get_tables",
     "pm_evaluate", "pm_evaluate_device", "pm_check_errors", "pm_set_eval_kernel",
     "pm_auto_eval_kernel", "pm_min_cost_sum", "pm_scan_depths_device", "pm_scan_walks_device", "pm_set_profiling",

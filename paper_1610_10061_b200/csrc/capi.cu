@@ -18,6 +18,14 @@ using namespace pmb;
 
 extern "C" {
 
+int pm_warmup(int device) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return PM_CUDA;
+  if (device < 0 || device >= ndev) return PM_DOMAIN;
+  if (cudaSetDevice(device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess) return PM_CUDA;
+  return PM_OK;
+}
+
 int pm_create(int device, pm_ctx** out) {
   if (!out) return PM_STRUCTURAL;
   *out = nullptr;
@@ -99,7 +107,10 @@ uint64_t pm_kernel_launches(const pm_ctx* c) { return c ? c->launches : 0; }
 
 static int bits_for(uint64_t v) { return v == 0 ? 0 : 64 - __builtin_clzll(v); }
 
-static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t m, size_t p) {
+// hcosts: the same matrix in host memory when the caller passed one (small
+// matrices are validated there: no kernel, no synchronisation)
+static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t m, size_t p,
+                             const int64_t* hcosts = nullptr) {
   // Instance::Instance checks, in the reference's order (instance.cpp:13-29).
   if (n == 0) return c->fail(PM_STRUCTURAL, "instance needs at least one client");
   if (m == 0) return c->fail(PM_STRUCTURAL, "instance needs at least one site");
@@ -108,16 +119,23 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   if (n > (size_t)INT_MAX / 2 || m > (size_t)INT_MAX / 2)
     return c->fail(PM_DOMAIN, "device tables support at most 2^30 clients and sites");
 
-  unsigned long long* scal = nullptr;
-  PM_CUDA_TRY(c, c->scal.ensure(16));
-  scal = c->scal.as<unsigned long long>();
-  PM_CUDA_TRY(c, cudaMemsetAsync(scal, 0, 16, c->stream));
-  PM_CUDA_TRY(c, launch_validate_costs(dcosts, n * m, scal, reinterpret_cast<int*>(scal + 1), c->sms,
-                                   c->stream));
-  c->launches += 1;
-  unsigned long long host[2] = {0, 0};
-  PM_CUDA_TRY(c, cudaMemcpyAsync(host, scal, 16, cudaMemcpyDeviceToHost, c->stream));
-  PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  unsigned long long host[2] = {0, 0};  // {max cost, negative seen}
+  if (hcosts && n * m <= ((size_t)1 << 20)) {
+    for (size_t x = 0; x < n * m; ++x) {
+      host[1] |= hcosts[x] < 0;
+      host[0] = std::max<unsigned long long>(host[0], hcosts[x] < 0 ? 0 : (unsigned long long)hcosts[x]);
+    }
+  } else {
+    unsigned long long* scal = nullptr;
+    PM_CUDA_TRY(c, c->scal.ensure(16));
+    scal = c->scal.as<unsigned long long>();
+    PM_CUDA_TRY(c, cudaMemsetAsync(scal, 0, 16, c->stream));
+    PM_CUDA_TRY(c, launch_validate_costs(dcosts, n * m, scal, reinterpret_cast<int*>(scal + 1), c->sms,
+                                         c->stream));
+    c->launches += 1;
+    PM_CUDA_TRY(c, cudaMemcpyAsync(host, scal, 16, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
   if (host[1] & 1) return c->fail(PM_STRUCTURAL, "costs must be non-negative");
   const int64_t max_cost = (int64_t)host[0];
   if (max_cost > 0 && max_cost > INT64_MAX / (int64_t)n)
@@ -171,10 +189,17 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   }
 
   c->has_instance = false;
-  c->ord.release();
-  c->dist.release();
-  c->dT.release();
   const size_t cells = n * (size_t)bp.Wp;
+  // tables are regrown only when they do not fit (a pooled context builds the
+  // next small instance without allocating); a large previous instance is
+  // dropped first so two never coexist
+  const size_t nP0 = (n + 15) / 16 * 16;
+  if (c->ord.bytes < cells * bp.site_bytes || c->dist.bytes < cells * bp.dist_bytes ||
+      c->dT.bytes < nP0 * m * (size_t)bp.dist_bytes || c->ord.bytes > ((size_t)256 << 20)) {
+    c->ord.release();
+    c->dist.release();
+    c->dT.release();
+  }
   PM_CUDA_TRY(c, c->ord.ensure(cells * bp.site_bytes));
   PM_CUDA_TRY(c, c->dist.ensure(cells * bp.dist_bytes));
   const size_t nP = (n + 15) / 16 * 16;
@@ -216,8 +241,8 @@ int pm_set_instance(pm_ctx* c, const int64_t* costs, size_t n, size_t m, size_t 
   if (n == 0 || m == 0 || p < 1 || p >= m) return set_instance_impl(c, nullptr, n, m, p);
   PM_CUDA_TRY(c, c->costs_in.ensure(n * m * 8));
   PM_CUDA_TRY(c, cudaMemcpyAsync(c->costs_in.p, costs, n * m * 8, cudaMemcpyHostToDevice, c->stream));
-  const int rc = set_instance_impl(c, c->costs_in.as<int64_t>(), n, m, p);
-  c->costs_in.release();
+  const int rc = set_instance_impl(c, c->costs_in.as<int64_t>(), n, m, p, costs);
+  if (c->costs_in.bytes > ((size_t)64 << 20)) c->costs_in.release();  // small staging is kept for the next call
   return rc;
 }
 
