@@ -64,7 +64,10 @@ typedef struct pm_table_info {
 /* ---- context ----------------------------------------------------------- */
 
 /* Initialises the CUDA runtime on `device` (the one-time context creation,
- * hundreds of milliseconds) without creating a pm_ctx; PM_CUDA without a device. */
+ * hundreds of milliseconds) without creating a pm_ctx; PM_CUDA without a device.
+ * As the process's first CUDA call it also selects eager module loading
+ * (CUDA_MODULE_LOADING=EAGER unless the caller set it), so no kernel pays its
+ * load time inside a timed call. */
 int pm_warmup(int device);
 /* Creates a context on CUDA device `device` with its own non-blocking stream. */
 int pm_create(int device, pm_ctx** out);

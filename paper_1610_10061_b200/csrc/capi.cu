@@ -6,6 +6,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +20,11 @@ using namespace pmb;
 extern "C" {
 
 int pm_warmup(int device) {
+  // load every kernel of the module with the context instead of at its first
+  // launch (lazy loading costs milliseconds per kernel inside the first timed
+  // call); only effective when this is the process's first CUDA call, and a
+  // caller's own CUDA_MODULE_LOADING wins
+  setenv("CUDA_MODULE_LOADING", "EAGER", 0);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return PM_CUDA;
   if (device < 0 || device >= ndev) return PM_DOMAIN;
