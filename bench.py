@@ -520,6 +520,12 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
                         else "torch.distributed gloo allgather")}
     if isinstance(ag, pm.NcclComm):
         ag.close()
+    if world == 1 and args.orlib_dir:
+        # BASELINE configs 1-2 on the real OR-Library files when supplied (tools/orlib_run.py)
+        import subprocess
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "orlib_run.py"), "--orlib-dir",
+                            args.orlib_dir, "--instances", "pmed1,pmed40"], capture_output=True, text=True)
+        out["orlib"] = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
     if world == 1 and rank == 0:
         # the paper's Table-1 shape (nb=60, nt=256) on a pmed40-sized synthetic instance
         import paper_1610_10061_b200 as pm2
@@ -699,6 +705,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-ga", action="store_true")
+    ap.add_argument("--orlib-dir", default=os.environ.get("PMB_ORLIB_DIR", ""),
+                    help="OR-Library pmed files + pmedopt: adds BASELINE configs 1-2 (pmed1, pmed40) to `ga`")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong (default): the BASELINE population split over the GPUs; weak: per GPU")
     args = ap.parse_args()
