@@ -77,7 +77,8 @@ void pm_destroy(pm_ctx* c) {
                     &c->costs_out, &c->T, &c->lists, &c->counts, &c->errw, &c->scal, &c->ga.pop,
                     &c->ga.next, &c->ga.cost, &c->ga.before, &c->ga.child, &c->ga.ccost, &c->ga.ok,
                     &c->ga.brec, &c->ga.evals, &c->ga.tmp, &c->ga.table, &c->ga.ranks, &c->ga.rflags,
-                    &c->ga.rstate, &c->ga.lfact, &c->ga.grec, &c->ga.gstate, &c->ga.perk, &c->sort_rows})
+                    &c->ga.rstate, &c->ga.lfact, &c->ga.grec, &c->ga.gstate, &c->ga.perk, &c->sort_rows,
+                    &c->c16, &c->dT16})
     b->release();
   c->ga.hrec.release();
   c->ga.hglob.release();
@@ -126,6 +127,11 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
     return c->fail(PM_DOMAIN, "device tables support at most 2^30 clients and sites");
 
   unsigned long long host[2] = {0, 0};  // {max cost, negative seen}
+  const size_t nP = (n + 15) / 16 * 16, mP = (m + 7) / 8 * 8;
+  // Large matrices: one fused pass validates and writes the u16 copies K1
+  // and K2b use (k_prep_costs), kept when every cost fits 16 bits.  Small
+  // host matrices are validated on the host (no kernel, no synchronisation).
+  bool prep = false;
   if (hcosts && n * m <= ((size_t)1 << 20)) {
     for (size_t x = 0; x < n * m; ++x) {
       host[1] |= hcosts[x] < 0;
@@ -136,12 +142,30 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
     PM_CUDA_TRY(c, c->scal.ensure(16));
     scal = c->scal.as<unsigned long long>();
     PM_CUDA_TRY(c, cudaMemsetAsync(scal, 0, 16, c->stream));
-    PM_CUDA_TRY(c, launch_validate_costs(dcosts, n * m, scal, reinterpret_cast<int*>(scal + 1), c->sms,
-                                         c->stream));
+    prep = getenv("PMB_K1_PREP") == nullptr || getenv("PMB_K1_PREP")[0] != '0';
+    // grow-only scratch, kept across instances of similar size (allocating
+    // and freeing gigabytes per call costs more than the kernels)
+    for (DevBuf* b : {&c->c16, &c->dT16})
+      if (b->bytes > 4 * (n * std::max(mP, nP) * 2) + (1 << 20)) b->release();
+    if (prep && (c->c16.ensure(n * mP * 2) != cudaSuccess || c->dT16.ensure(m * nP * 2) != cudaSuccess)) {
+      (void)cudaGetLastError();  // not enough memory for the copies: the three-pass path
+      c->c16.release();
+      c->dT16.release();
+      prep = false;
+    }
+    if (prep) {
+      PM_CUDA_TRY(c, launch_prep_costs(dcosts, (int)n, (int)m, (int)mP, (int)nP, c->c16.as<uint16_t>(),
+                                       c->dT16.as<uint16_t>(), scal, reinterpret_cast<int*>(scal + 1), c->sms,
+                                       c->stream));
+    } else {
+      PM_CUDA_TRY(c, launch_validate_costs(dcosts, n * m, scal, reinterpret_cast<int*>(scal + 1), c->sms,
+                                           c->stream));
+    }
     c->launches += 1;
     PM_CUDA_TRY(c, cudaMemcpyAsync(host, scal, 16, cudaMemcpyDeviceToHost, c->stream));
     PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   }
+  if (prep && host[0] > 65535) prep = false;  // the speculative u16 copies do not hold these costs
   if (host[1] & 1) return c->fail(PM_STRUCTURAL, "costs must be non-negative");
   const int64_t max_cost = (int64_t)host[0];
   if (max_cost > 0 && max_cost > INT64_MAX / (int64_t)n)
@@ -153,6 +177,7 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   bp.p = (int)p;
   bp.W = (int)(m - p + 1);
   bp.Wp = (bp.W + 15) / 16 * 16;
+  bp.mP = (int)mP;
   bp.site_bytes = m <= 65535 ? 2 : 4;  // sentinel site m must fit
   bp.dist_bytes = max_cost <= 65535 ? 2 : (max_cost <= 0xffffffffLL ? 4 : 8);
   bp.sitebits = std::max(1, bits_for((uint64_t)(m - 1)));
@@ -199,21 +224,27 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   // tables are regrown only when they do not fit (a pooled context builds the
   // next small instance without allocating); a large previous instance is
   // dropped first so two never coexist
-  const size_t nP0 = (n + 15) / 16 * 16;
-  if (c->ord.bytes < cells * bp.site_bytes || c->dist.bytes < cells * bp.dist_bytes ||
-      c->dT.bytes < nP0 * m * (size_t)bp.dist_bytes || c->ord.bytes > ((size_t)256 << 20)) {
+  // (regrown when too small, or dropped when more than 4x the need: a large
+  // instance's tables do not linger behind a small one)
+  auto fits = [](const DevBuf& b, size_t need) { return b.bytes >= need && b.bytes <= 4 * need + (1 << 20); };
+  if (!fits(c->ord, cells * bp.site_bytes) || !fits(c->dist, cells * bp.dist_bytes)) {
     c->ord.release();
     c->dist.release();
-    c->dT.release();
   }
+  if (!prep && !fits(c->dT, nP * m * (size_t)bp.dist_bytes)) c->dT.release();
   PM_CUDA_TRY(c, c->ord.ensure(cells * bp.site_bytes));
   PM_CUDA_TRY(c, c->dist.ensure(cells * bp.dist_bytes));
-  const size_t nP = (n + 15) / 16 * 16;
-  PM_CUDA_TRY(c, c->dT.ensure(nP * m * (size_t)bp.dist_bytes));
-  PM_CUDA_TRY(c, launch_build_rows(bp, dcosts, c->ord.p, c->dist.p, c->sort_keys.p,
+  const uint16_t* c16 = prep && bp.dist_bytes == 2 ? c->c16.as<uint16_t>() : nullptr;
+  PM_CUDA_TRY(c, launch_build_rows(bp, dcosts, c16, c->ord.p, c->dist.p, c->sort_keys.p,
                                    c->sort_pay.as<uint32_t>(), c->sort_rows.as<int>(), c->stream));
-  PM_CUDA_TRY(c, launch_transpose_costs(dcosts, (int)n, (int)nP, (int)m, bp.dist_bytes, c->dT.p, c->stream));
-  c->launches += 2;
+  if (prep) {  // the u16 site-major table is already built: adopt it (the old one becomes scratch)
+    std::swap(c->dT, c->dT16);
+  } else {
+    PM_CUDA_TRY(c, c->dT.ensure(nP * m * (size_t)bp.dist_bytes));
+    PM_CUDA_TRY(c, launch_transpose_costs(dcosts, (int)n, (int)nP, (int)m, bp.dist_bytes, c->dT.p, c->stream));
+    c->launches += 1;
+  }
+  c->launches += 1;
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (!bp.smem_path) {
     c->sort_keys.release();
@@ -233,8 +264,9 @@ static int set_instance_impl(pm_ctx* c, const int64_t* dcosts, size_t n, size_t 
   t.ord = c->ord.p;
   t.dist = c->dist.p;
   t.dT = c->dT.p;
-  t.nP = (int)((n + 15) / 16 * 16);
-  c->open_cap = (int)std::min<size_t>(m, (std::max<size_t>(p, 16) + 3) / 4 * 4);
+  t.nP = (int)nP;
+  // a multiple of 4: the gather reads the lists 16 bytes at a time
+  c->open_cap = (int)((std::min<size_t>(m, std::max<size_t>(p, 16)) + 3) / 4 * 4);
   c->has_instance = true;
   c->err.clear();
   return PM_OK;

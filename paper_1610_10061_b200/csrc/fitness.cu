@@ -101,6 +101,20 @@ cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int
 // ---- K2: bit-sliced scan -------------------------------------------------------
 
 constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
+// A/B switches for K2 variants (tools/build_variant.sh); defaults are the
+// measured choice (profiles/r02_k2_ab.md: every switch on is slower at syn20k)
+#ifndef PMB_X_SPLITQ
+#define PMB_X_SPLITQ 0
+#endif
+#ifndef PMB_X_BFIND
+#define PMB_X_BFIND 0
+#endif
+#ifndef PMB_X_NOSENT
+#define PMB_X_NOSENT 0
+#endif
+#ifndef PMB_X_RED
+#define PMB_X_RED 0
+#endif
 constexpr int kWideWarps = 24, kWideQueue = 256;  // the many-warp K2 variant (plan_scan)
 #ifndef PMB_QCHECK
 #define PMB_QCHECK 2
@@ -134,6 +148,12 @@ struct Chunk {
     if constexpr (sizeof(OrdT) == 2) return (w[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
     else return w[j];
   }
+  // u16 costs: the 32-bit word holding column j's cost in its low 16 bits
+  // (the high half is the next column's cost for even j)
+  __device__ __forceinline__ uint32_t cost_raw(int j) const {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(d);
+    return (j & 1) ? (w[j >> 1] >> 16) : w[j >> 1];
+  }
   __device__ __forceinline__ uint64_t cost(int j) const {
     const uint32_t* w = reinterpret_cast<const uint32_t*>(d);
     if constexpr (sizeof(DistT) == 2) return (w[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
@@ -151,7 +171,12 @@ struct MaskOps {
   static constexpr int kG = 8 * sizeof(MaskT);
   __device__ __forceinline__ static int pop_high(MaskT& h) {  // index of the top set bit, cleared
     if constexpr (sizeof(MaskT) == 4) {
+#if PMB_X_BFIND
+      int c;
+      asm("bfind.u32 %0, %1;" : "=r"(c) : "r"(h));  // FLO: the top bit's position directly
+#else
       const int c = 31 - __clz(h);
+#endif
       h ^= 1u << c;
       return c;
     } else {
@@ -203,15 +228,19 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = lanemask_lt();
   AccT* myacc = acc + (size_t)warp * kG * 32 + lane;
-  // the warp's queue of hit columns (at most kChunk * 32 per chunk); a 32-bit
-  // mask and a 32-bit cost share one 8-byte record (one STS / LDS)
+  // the warp's queue of hit columns (at most kChunk * 32 per chunk).  32-bit
+  // masks and costs: one [mask x kQ | cost x kQ] region per warp, so both
+  // stores of a record share one address register (immediate offset kQ * 4)
+  // and need no register pair; otherwise separate [warp][kQ] arrays.
   constexpr bool kPacked = sizeof(MaskT) == 4 && sizeof(AccT) == 4;
-  MaskT* wqh = hbuf + (size_t)warp * kQ;
-  AccT* wqd = dbuf + (size_t)warp * kQ;
-  uint64_t* wq = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kQ;
-  (void)wqh;
-  (void)wqd;
+  MaskT* wqh = kPacked ? hbuf + (size_t)warp * 2 * kQ : hbuf + (size_t)warp * kQ;
+  AccT* wqd = kPacked ? reinterpret_cast<AccT*>(wqh + kQ) : dbuf + (size_t)warp * kQ;
+  uint64_t* wq = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kQ;  // one 8-byte record (!PMB_X_SPLITQ)
   (void)wq;
+  // u16 sorted distances: a record of an even column stores the raw 32-bit
+  // word holding the column's cost in its low half (no extraction in the
+  // column loop); the drain masks it
+  constexpr bool kRawCost = PMB_X_SPLITQ && !kDepth && sizeof(DistT) == 2 && sizeof(AccT) == 4;
 
   const long long U = (long long)groups * n;
   long long u = U * blockIdx.x / gridDim.x;
@@ -324,7 +353,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
           MaskT h = 0;
           AccT dv = 0;
           if (base + lane < qn) {
-            if constexpr (kPacked) {
+            if constexpr (kPacked && !PMB_X_SPLITQ) {
               const uint64_t x = wq[base + lane];
               h = (MaskT)x;
               dv = (AccT)(x >> 32);
@@ -332,10 +361,18 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
               h = wqh[base + lane];
               dv = wqd[base + lane];
             }
+            if constexpr (kRawCost) dv &= 0xffffu;
           }
           while (h) {
             const int c = Ops::pop_high(h);
+#if PMB_X_RED
+            // a shared-memory reduction: lane-private column (no contention),
+            // and the lane does not wait for a load-add-store round trip
+            if constexpr (sizeof(AccT) == 4) atomicAdd(reinterpret_cast<unsigned*>(myacc + c * 32), (unsigned)dv);
+            else atomicAdd(reinterpret_cast<unsigned long long*>(myacc + c * 32), (unsigned long long)dv);
+#else
             myacc[c * 32] += dv;
+#endif
           }
         }
         __syncwarp();  // the queue is rewritten next
@@ -356,10 +393,13 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
         if (h) {
           // kDepth: the 1-based stopping column k* instead of the cost
           // (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
-          const AccT dval = kDepth ? (AccT)(k + j + 1) : (AccT)cur.cost(j);
+          AccT dval;
+          if constexpr (kDepth) dval = (AccT)(k + j + 1);
+          else if constexpr (kRawCost) dval = (AccT)cur.cost_raw(j);
+          else dval = (AccT)cur.cost(j);
           const uint32_t q = qn + __popc(hb & lt);
           PMB_CHECK(q < (uint32_t)kQ);
-          if constexpr (kPacked) {
+          if constexpr (kPacked && !PMB_X_SPLITQ) {
             wq[q] = (uint64_t)h | ((uint64_t)dval << 32);
           } else {
             wqh[q] = h;
@@ -374,10 +414,12 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
         if (alive == 0 || k >= Wp) {
           if (alive) atomicMin(err, (unsigned long long)g * kG + Ops::low_index(alive));
           i = -1;
-          alive = 0;
+          alive = 0;  // the idle lane's stale chunks keep valid site indices (< Ts): its lookups never hit
+#if !PMB_X_NOSENT
           cur.set_sentinel(sentinel);
           nxt.set_sentinel(sentinel);
           nxt2.set_sentinel(sentinel);
+#endif
         } else if (k + (kBufs - 1) * kChunk < Wp) {
           PMB_CHECK(k + kBufs * kChunk <= Wp);
           cur.load(orow, drow, k + (kBufs - 1) * kChunk);
@@ -739,16 +781,35 @@ __global__ void __launch_bounds__(kGatherThreads)
         const uint32_t* list = lists + c * (size_t)cap;
         uint32_t t = 0;
         PMB_CHECK(i0 + V <= nP && pc <= (uint32_t)cap);
-        for (; t + 4 <= pc; t += 4) {
-          uint4 x[4];
+        // 8 open sites per step: their indices arrive as two 16-byte loads
+        // (lists are 16-byte aligned, cap % 4 == 0) and the 8 client-vector
+        // loads are all in flight before the first min (the kernel is bound by
+        // L2 latency, not bandwidth)
+        for (; t + 8 <= pc; t += 8) {
+          const uint4 ja = __ldg(reinterpret_cast<const uint4*>(list + t));
+          const uint4 jb = __ldg(reinterpret_cast<const uint4*>(list + t + 4));
+          const uint32_t js[8] = {ja.x, ja.y, ja.z, ja.w, jb.x, jb.y, jb.z, jb.w};
+          uint4 x[8];
 #ifdef PMB_BOUNDS
-          for (int u = 0; u < 4; ++u) PMB_CHECK(list[t + u] < (uint32_t)m);
+          for (int u = 0; u < 8; ++u) PMB_CHECK(js[u] < (uint32_t)m);
 #endif
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            x[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)__ldg(list + t + u) * nP));
+          for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)js[u] * nP));
+#pragma unroll
+          for (int u = 0; u < 8; ++u) best.min_with(x[u]);
+        }
+        if (t + 4 <= pc) {
+          const uint4 ja = __ldg(reinterpret_cast<const uint4*>(list + t));
+          const uint32_t js[4] = {ja.x, ja.y, ja.z, ja.w};
+          uint4 x[4];
+#ifdef PMB_BOUNDS
+          for (int u = 0; u < 4; ++u) PMB_CHECK(js[u] < (uint32_t)m);
+#endif
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)js[u] * nP));
 #pragma unroll
           for (int u = 0; u < 4; ++u) best.min_with(x[u]);
+          t += 4;
         }
         for (; t < pc; ++t) best.min_with(__ldg(reinterpret_cast<const uint4*>(col + (size_t)__ldg(list + t) * nP)));
 #pragma unroll

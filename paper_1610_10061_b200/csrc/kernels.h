@@ -14,6 +14,7 @@ enum class KeyKind { kPacked32, kPacked64, kPayload64 };
 // K1 launch plan, chosen by the host from the validated instance.
 struct BuildPlan {
   int n = 0, m = 0, p = 0, W = 0, Wp = 0;
+  int mP = 0;  // row stride of the u16 cost copy (round_up(m, 8))
   int site_bytes = 4, dist_bytes = 8;
   int sitebits = 0, costbits = 0, npasses = 0;
   KeyKind key_kind = KeyKind::kPacked64;
@@ -31,8 +32,14 @@ cudaError_t launch_validate_costs(const int64_t* costs, size_t count, unsigned l
                               int* out_neg, int sms, cudaStream_t st);
 // rows: device int[1 + n] (count, then the rows the counting-sort path hands
 // to the radix kernel); used only when bp.cs_path
-cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
+// c16: the u16 copy of the matrix (row stride bp.mP) when every cost fits 16
+// bits and the tables are u16, else nullptr (rows come from the int64 matrix)
+cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, const uint16_t* c16, void* ord, void* dist,
                               void* scratch_keys, uint32_t* scratch_pay, int* rows, cudaStream_t st);
+// One pass over the int64 matrix: max cost / negativity into out_max / out_neg
+// (zeroed by the caller) and the speculative u16 copies c16 (n x mP) and dT (m x nP).
+cudaError_t launch_prep_costs(const int64_t* costs, int n, int m, int mP, int nP, uint16_t* c16, uint16_t* dT,
+                              unsigned long long* out_max, int* out_neg, int sms, cudaStream_t st);
 cudaError_t launch_transpose_costs(const int64_t* costs, int n, int nP, int m, int dist_bytes, void* dT,
                                    cudaStream_t st);
 

@@ -53,6 +53,84 @@ __global__ void k_validate_costs(const int64_t* __restrict__ costs, size_t count
   }
 }
 
+// ---- one pass over the int64 matrix: validation + the narrow copies ------
+//
+// Instance validation (instance.cpp:20-29: max cost, negativity) fused with
+// the two narrow copies the device path keeps, written speculatively at u16
+// (valid when the max cost fits, which the host checks from the same pass):
+//   c16[i][j] = cost(i, j), row stride mP = round_up(m, 8) -- K1's input, a
+//               quarter of the int64 bytes, 16-byte vector loads per row;
+//   dT[j][i]  = cost(i, j), row stride nP -- the gather kernel's site-major table.
+// So the 8-byte matrix is read from HBM once (previously three times:
+// validation, K1, transpose).  32 x 32 tiles through shared memory; a
+// persistent grid keeps one max / flag per CTA.
+__global__ void __launch_bounds__(256) k_prep_costs(const int64_t* __restrict__ costs, int n, int m, int mP, int nP,
+                                                    uint16_t* __restrict__ c16, uint16_t* __restrict__ dT,
+                                                    unsigned long long* __restrict__ out_max,
+                                                    int* __restrict__ out_neg) {
+  // 64 rows x 32 columns per tile: 8 independent 8-byte loads per thread in
+  // flight (enough bytes in flight per SM to stream HBM)
+  constexpr int kR = 64;
+  __shared__ uint16_t tile[kR][34];  // 17 words per row: transposed reads hit distinct banks
+  __shared__ unsigned long long smax[8];
+  __shared__ int sneg[8];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int tilesX = (m + 31) / 32, tilesY = (nP + kR - 1) / kR;
+  const long long total = (long long)tilesX * tilesY;
+  int64_t mx = 0;
+  int neg = 0;
+  for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+    const int i0 = (int)(t / tilesX) * kR, j0 = (int)(t % tilesX) * 32;
+    const int j = j0 + tx;
+    int64_t v[kR / 8];
+#pragma unroll
+    for (int q = 0; q < kR / 8; ++q) {
+      const int i = i0 + ty + 8 * q;
+      v[q] = (i < n && j < m) ? __ldg(costs + (size_t)i * m + j) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kR / 8; ++q) {
+      const int r = ty + 8 * q, i = i0 + r;
+      mx = v[q] > mx ? v[q] : mx;
+      neg |= v[q] < 0;
+      const uint16_t u = (uint16_t)v[q];
+      if (i < n && j < m) c16[(size_t)i * mP + j] = u;
+      tile[r][tx] = u;
+    }
+    __syncthreads();
+    // transposed: 32 sites x 64 clients, two clients per thread (4-byte stores)
+    for (int r = ty; r < 32; r += 8) {
+      const int jj = j0 + r, i = i0 + 2 * tx;
+      if (jj < m && i < nP) {
+        const uint32_t pair = (uint32_t)tile[2 * tx][r] | ((uint32_t)tile[2 * tx + 1][r] << 16);
+        *reinterpret_cast<uint32_t*>(dT + (size_t)jj * nP + i) = pair;  // nP % 16 == 0, i even
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t v = __shfl_xor_sync(kFull, mx, o);
+    mx = v > mx ? v : mx;
+  }
+  neg = __any_sync(kFull, neg);
+  if (tx == 0) {
+    smax[ty] = (unsigned long long)mx;
+    sneg[ty] = neg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = 0;
+    int ng = 0;
+    for (int w = 0; w < 8; ++w) {
+      b = smax[w] > b ? smax[w] : b;
+      ng |= sneg[w];
+    }
+    atomicMax(out_max, b);
+    if (ng) atomicOr(out_neg, 1);
+  }
+}
+
 // ---- K1: per-row stable radix sort ----------------------------------------
 
 constexpr int kSortThreads = 1024;
@@ -258,9 +336,9 @@ __device__ __forceinline__ unsigned digit_peers(unsigned d, bool valid, int nbit
   return peers;
 }
 
-template <class KeyT, class OrdT, class DistT, bool kSmem>
+template <class KeyT, class OrdT, class DistT, bool kSmem, class CostT>
 __global__ void __launch_bounds__(kSortThreads, 1)
-    k_build_rows_ws(const int64_t* __restrict__ costs, int n, int m, int W, int Wp, int sitebits,
+    k_build_rows_ws(const CostT* __restrict__ costs, int cstride, int n, int m, int W, int Wp, int sitebits,
                     int npasses, int dbits, OrdT* __restrict__ ord, DistT* __restrict__ dist,
                     KeyT* __restrict__ gkeys, const int* __restrict__ rows) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -282,7 +360,7 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   const int nr = rows ? rows[0] : n;
   for (int ri = blockIdx.x; ri < nr; ri += gridDim.x) {
     const int r = rows ? rows[1 + ri] : ri;
-    const int64_t* crow = costs + (size_t)r * m;
+    const CostT* crow = costs + (size_t)r * cstride;
     // keys of the warp's slice, with the first pass's digit histogram (shared
     // atomics: one per key, instead of a ballot ranking pass)
     for (int d = lane; d < 256; d += 32) mycnt[d] = 0;
@@ -382,17 +460,39 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 // arbitrary order, so each bucket is then put back into ascending site order
 // (the reference's tie-break, ordering.cpp:25-28) by its owning thread with an
 // insertion sort -- buckets are the sites at one exact cost, a handful for
-// metric instances.  A row with a bucket above kCsMaxBucket is handed back
+// metric instances.  (That sort is 70 % of the kernel's instructions at
+// syn20k; ranking every element within its bucket instead measured slower,
+// 2.88 -> 2.98 ms: it scans the whole bucket per element.)  A row with a bucket above kCsMaxBucket is handed back
 // (rows list) to the radix kernel, so adversarial ties cost radix time, never
 // quadratic time.  512-thread CTAs, two per SM when the row fits in half the
 // shared memory: one CTA's HBM row load overlaps the other's sort.
 constexpr int kCsThreads = 512;
 constexpr uint32_t kCsMaxBucket = 64;
 
-template <class OrdT, class DistT>
+// Every (site, cost) of row `crow`: 16-byte loads of 8 u16 costs (the padded
+// u16 copy) or one int64 per element.
+template <class CostT, class F>
+__device__ __forceinline__ void for_each_cost(const CostT* __restrict__ crow, int m, int tid, F&& f) {
+  if constexpr (sizeof(CostT) == 2) {
+    const uint4* v = reinterpret_cast<const uint4*>(crow);
+    for (int x8 = tid; x8 * 8 < m; x8 += kCsThreads) {
+      const uint4 w = __ldg(v + x8);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int x = x8 * 8 + q;
+        if (x < m) f(x, (ws[q >> 1] >> ((q & 1) * 16)) & 0xffffu);
+      }
+    }
+  } else {
+    for (int x = tid; x < m; x += kCsThreads) f(x, (uint32_t)crow[x]);
+  }
+}
+
+template <class OrdT, class DistT, class CostT>
 __global__ void __launch_bounds__(kCsThreads, 2)
-    k_build_rows_cs(const int64_t* __restrict__ costs, int n, int m, int W, int Wp, int sitebits, int costbits,
-                    OrdT* __restrict__ ord, DistT* __restrict__ dist, int* __restrict__ rows) {
+    k_build_rows_cs(const CostT* __restrict__ costs, int cstride, int n, int m, int W, int Wp, int sitebits,
+                    int costbits, OrdT* __restrict__ ord, DistT* __restrict__ dist, int* __restrict__ rows) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t wsum[kCsThreads / 32];
   __shared__ int flag;
@@ -404,14 +504,11 @@ __global__ void __launch_bounds__(kCsThreads, 2)
   const int per = (nw + kCsThreads - 1) / kCsThreads;  // counter words owned by a thread in the scan
   const int w0 = min(nw, tid * per), w1 = min(nw, w0 + per);
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
-    const int64_t* crow = costs + (size_t)r * m;
+    const CostT* crow = costs + (size_t)r * cstride;
     for (int x = tid; x < nw; x += kCsThreads) cnt[x] = 0;
     if (tid == 0) flag = 0;
     __syncthreads();
-    for (int x = tid; x < m; x += kCsThreads) {
-      const uint32_t c = (uint32_t)crow[x];
-      atomicAdd(&cnt[c >> 1], 1u << ((c & 1) << 4));
-    }
+    for_each_cost(crow, m, tid, [&](int, uint32_t c) { atomicAdd(&cnt[c >> 1], 1u << ((c & 1) << 4)); });
     __syncthreads();
     // exclusive scan over the buckets (each thread a contiguous run of words)
     uint32_t sum = 0;
@@ -453,12 +550,11 @@ __global__ void __launch_bounds__(kCsThreads, 2)
       if (tid == 0) rows[1 + atomicAdd(rows, 1)] = r;
       continue;  // the next row's first barrier orders the reuse of cnt / flag
     }
-    for (int x = tid; x < m; x += kCsThreads) {  // scatter through atomic cursors
-      const uint32_t c = (uint32_t)crow[x];
+    for_each_cost(crow, m, tid, [&](int x, uint32_t c) {  // scatter through atomic cursors
       const uint32_t sh = (c & 1) << 4;
       const uint32_t old = atomicAdd(&cnt[c >> 1], 1u << sh);
       out[(old >> sh) & 0xffffu] = (c << sitebits) | (uint32_t)x;
-    }
+    });
     __syncthreads();
     for (int b = tid; b < nb; b += kCsThreads) {  // bucket b = [end(b-1), end(b)), cursors now at the ends
       const uint32_t e = (cnt[b >> 1] >> ((b & 1) << 4)) & 0xffffu;
@@ -520,6 +616,14 @@ __global__ void k_transpose_costs(const int64_t* __restrict__ costs, int n, int 
 
 // ---- host launchers --------------------------------------------------------
 
+cudaError_t launch_prep_costs(const int64_t* costs, int n, int m, int mP, int nP, uint16_t* c16, uint16_t* dT,
+                              unsigned long long* out_max, int* out_neg, int sms, cudaStream_t st) {
+  const long long tiles = (long long)((m + 31) / 32) * ((nP + 63) / 64);
+  const int blocks = (int)std::min<long long>((long long)sms * 8, tiles);
+  k_prep_costs<<<blocks, 256, 0, st>>>(costs, n, m, mP, nP, c16, dT, out_max, out_neg);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_validate_costs(const int64_t* costs, size_t count, unsigned long long* out_max,
                               int* out_neg, int sms, cudaStream_t st) {
   const int blocks = (int)std::min<size_t>((size_t)sms * 8, (count + 255) / 256 + 1);
@@ -530,20 +634,28 @@ cudaError_t launch_validate_costs(const int64_t* costs, size_t count, unsigned l
 size_t sort_smem_header() { return ((256 + 256 + 256 * kHistPitch + 4) * 4 + 15) / 16 * 16; }
 
 template <class KeyT, bool kPayload, class OrdT, class DistT>
-static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
-                                 void* scratch_keys, uint32_t* scratch_pay, int* rows, cudaStream_t st) {
+static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, const uint16_t* c16, void* ord,
+                                 void* dist, void* scratch_keys, uint32_t* scratch_pay, int* rows, cudaStream_t st) {
   const size_t per = (size_t)bp.m * (sizeof(KeyT) + (kPayload ? 4 : 0)) * 2;
   const size_t smem = sort_smem_header() + per;
   if constexpr (!kPayload && sizeof(KeyT) == 4 && sizeof(OrdT) == 2) {
     if (bp.cs_path) {  // counting sort; rows with large tie buckets go to the radix kernel below
       const size_t cs = cs_smem(bp.m, bp.cs_bits);
-      auto kern = k_build_rows_cs<OrdT, DistT>;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+      cudaError_t e = cudaMemsetAsync(rows, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
-      e = cudaMemsetAsync(rows, 0, sizeof(int), st);
-      if (e != cudaSuccess) return e;
-      kern<<<bp.cs_grid, kCsThreads, cs, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.cs_bits,
-                                                (OrdT*)ord, (DistT*)dist, rows);
+      if (c16) {
+        auto kern = k_build_rows_cs<OrdT, DistT, uint16_t>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+        if (e != cudaSuccess) return e;
+        kern<<<bp.cs_grid, kCsThreads, cs, st>>>(c16, bp.mP, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.cs_bits,
+                                                  (OrdT*)ord, (DistT*)dist, rows);
+      } else {
+        auto kern = k_build_rows_cs<OrdT, DistT, int64_t>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+        if (e != cudaSuccess) return e;
+        kern<<<bp.cs_grid, kCsThreads, cs, st>>>(costs, bp.m, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.cs_bits,
+                                                  (OrdT*)ord, (DistT*)dist, rows);
+      }
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
@@ -553,21 +665,27 @@ static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void
     // ballot per digit bit in the ranking), e.g. 2 x 7 bits for 14-bit costs
     const int dbits = bp.npasses ? (bp.costbits + bp.npasses - 1) / bp.npasses : 8;
     const size_t hs = sort_smem_header();
-    if (bp.smem_path) {
-      auto kern = k_build_rows_ws<KeyT, OrdT, DistT, true>;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto go = [&](auto kern, size_t sm, KeyT* keys) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
-      kern<<<bp.grid, kSortThreads, smem, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.npasses, dbits,
-                                                (OrdT*)ord, (DistT*)dist, nullptr, bp.cs_path ? rows : nullptr);
-    } else {
-      auto kern = k_build_rows_ws<KeyT, OrdT, DistT, false>;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
+      if (c16)
+        kern<<<bp.grid, kSortThreads, sm, st>>>(c16, bp.mP, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.npasses, dbits,
+                                                (OrdT*)ord, (DistT*)dist, keys, bp.cs_path ? rows : nullptr);
+      return cudaGetLastError();
+    };
+    auto go64 = [&](auto kern, size_t sm, KeyT* keys) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
-      kern<<<bp.grid, kSortThreads, hs, st>>>(costs, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.npasses, dbits,
-                                              (OrdT*)ord, (DistT*)dist, (KeyT*)scratch_keys,
-                                              bp.cs_path ? rows : nullptr);
+      kern<<<bp.grid, kSortThreads, sm, st>>>(costs, bp.m, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.npasses, dbits,
+                                              (OrdT*)ord, (DistT*)dist, keys, bp.cs_path ? rows : nullptr);
+      return cudaGetLastError();
+    };
+    if (c16) {
+      return bp.smem_path ? go(k_build_rows_ws<KeyT, OrdT, DistT, true, uint16_t>, smem, nullptr)
+                          : go(k_build_rows_ws<KeyT, OrdT, DistT, false, uint16_t>, hs, (KeyT*)scratch_keys);
     }
-    return cudaGetLastError();
+    return bp.smem_path ? go64(k_build_rows_ws<KeyT, OrdT, DistT, true, int64_t>, smem, nullptr)
+                        : go64(k_build_rows_ws<KeyT, OrdT, DistT, false, int64_t>, hs, (KeyT*)scratch_keys);
   }
   if (bp.smem_path) {
     auto kern = k_build_rows<KeyT, kPayload, OrdT, DistT, true>;
@@ -588,28 +706,28 @@ static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, void
 }
 
 template <class OrdT, class DistT>
-static cudaError_t launch_rows_od(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
-                                  void* sk, uint32_t* sp, int* rows, cudaStream_t st) {
+static cudaError_t launch_rows_od(const BuildPlan& bp, const int64_t* costs, const uint16_t* c16, void* ord,
+                                  void* dist, void* sk, uint32_t* sp, int* rows, cudaStream_t st) {
   switch (bp.key_kind) {
     case KeyKind::kPacked32:
-      return launch_rows_t<uint32_t, false, OrdT, DistT>(bp, costs, ord, dist, sk, sp, rows, st);
+      return launch_rows_t<uint32_t, false, OrdT, DistT>(bp, costs, c16, ord, dist, sk, sp, rows, st);
     case KeyKind::kPacked64:
-      return launch_rows_t<uint64_t, false, OrdT, DistT>(bp, costs, ord, dist, sk, sp, rows, st);
-    default:
-      return launch_rows_t<uint64_t, true, OrdT, DistT>(bp, costs, ord, dist, sk, sp, rows, st);
+      return launch_rows_t<uint64_t, false, OrdT, DistT>(bp, costs, c16, ord, dist, sk, sp, rows, st);
+    default:  // payload keys: costs wider than 64 - sitebits bits, never the u16 copy
+      return launch_rows_t<uint64_t, true, OrdT, DistT>(bp, costs, nullptr, ord, dist, sk, sp, rows, st);
   }
 }
 
-cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, void* ord, void* dist,
-                              void* scratch_keys, uint32_t* scratch_pay, int* rows, cudaStream_t st) {
+cudaError_t launch_build_rows(const BuildPlan& bp, const int64_t* costs, const uint16_t* c16, void* ord,
+                              void* dist, void* scratch_keys, uint32_t* scratch_pay, int* rows, cudaStream_t st) {
   if (bp.site_bytes == 2) {
-    if (bp.dist_bytes == 2) return launch_rows_od<uint16_t, uint16_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
-    if (bp.dist_bytes == 4) return launch_rows_od<uint16_t, uint32_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
-    return launch_rows_od<uint16_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
+    if (bp.dist_bytes == 2) return launch_rows_od<uint16_t, uint16_t>(bp, costs, c16, ord, dist, scratch_keys, scratch_pay, rows, st);
+    if (bp.dist_bytes == 4) return launch_rows_od<uint16_t, uint32_t>(bp, costs, nullptr, ord, dist, scratch_keys, scratch_pay, rows, st);
+    return launch_rows_od<uint16_t, uint64_t>(bp, costs, nullptr, ord, dist, scratch_keys, scratch_pay, rows, st);
   }
-  if (bp.dist_bytes == 2) return launch_rows_od<uint32_t, uint16_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
-  if (bp.dist_bytes == 4) return launch_rows_od<uint32_t, uint32_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
-  return launch_rows_od<uint32_t, uint64_t>(bp, costs, ord, dist, scratch_keys, scratch_pay, rows, st);
+  if (bp.dist_bytes == 2) return launch_rows_od<uint32_t, uint16_t>(bp, costs, c16, ord, dist, scratch_keys, scratch_pay, rows, st);
+  if (bp.dist_bytes == 4) return launch_rows_od<uint32_t, uint32_t>(bp, costs, nullptr, ord, dist, scratch_keys, scratch_pay, rows, st);
+  return launch_rows_od<uint32_t, uint64_t>(bp, costs, nullptr, ord, dist, scratch_keys, scratch_pay, rows, st);
 }
 
 cudaError_t launch_transpose_costs(const int64_t* costs, int n, int nP, int m, int dist_bytes, void* dT,
