@@ -434,14 +434,20 @@ class Context:
                                           first_block, bc.ctypes.data, bt.ctypes.data))
         return b, bc[:nb], bt[:nb].astype(np.int64)
 
-    def run_ga(self, cfg: GaConfig, rank: int = 0, world: int = 1, allgather=None):
+    def run_ga(self, cfg: GaConfig, rank: int = 0, world: int = 1, allgather=None, allgather_device=None):
         """pmedian::run_ga -> dict with the RunResult fields (ga.hpp:49-56) and work counters.
         allgather: None (one island), a NcclComm (the library's device NCCL exchange,
-        records never leave the GPU) or a pm_allgather_fn-shaped host callable."""
+        records never leave the GPU) or a pm_allgather_fn-shaped host callable;
+        allgather_device: a pm_allgather_device_fn-shaped callable
+        (send_dev, bytes, recv_dev, stream, user) that gathers device buffers."""
         wp = words_per(self.m)
         best = np.zeros(wp, dtype=np.uint64)
         r = _RunResult()
-        if world == 1 and allgather is None:
+        if allgather_device is not None:
+            cb = ALLGATHER_DEVICE_FN(allgather_device)
+            rc = _lib.pm_run_ga_islands_device(self._h, C.byref(cfg), rank, world, C.cast(cb, _vp), None,
+                                               best.ctypes.data, None, C.byref(r))
+        elif world == 1 and allgather is None:
             rc = _lib.pm_run_ga(self._h, C.byref(cfg), best.ctypes.data, None, C.byref(r))
         elif isinstance(allgather, NcclComm):  # the library's own NCCL exchange, no Python in the loop
             rc = _lib.pm_run_ga_islands_device(self._h, C.byref(cfg), rank, world, _NCCL_ALLGATHER_DEVICE,

@@ -115,3 +115,73 @@ def test_native_nccl_exchange_single_rank():
     assert (a["per_kernel_best_costs"] == b["per_kernel_best_costs"]).all()
     comm.close()
     ctx.close()
+
+
+def _device_ring(world):
+    """An in-process stand-in for a device all-gather (pm_allgather_device_fn)
+    between `world` contexts on one GPU: each rank copies its device record into
+    every rank's device receive buffer (cudaMemcpy, peer-free on one device);
+    host barriers order the copies -- no kernel waits on another rank."""
+    import threading
+
+    from cuda.bindings import runtime as rt
+    bar = threading.Barrier(world)
+    recv = [None] * world
+
+    def make(rank):
+        def fn(send, nbytes, recv_dev, stream, _user):
+            try:
+                rt.cudaStreamSynchronize(stream)  # this rank's records are written
+                recv[rank] = recv_dev
+                bar.wait()
+                for r2 in range(world):
+                    (err,) = rt.cudaMemcpy(recv[r2] + rank * nbytes, send, nbytes,
+                                           rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+                    if err != rt.cudaError_t.cudaSuccess:
+                        return 1
+                bar.wait()  # every rank's buffer is complete before any step kernel reads it
+                return 0
+            except Exception:
+                return 1
+        return fn
+    return [make(r) for r in range(world)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,team", [(2, False), (4, False), (2, True)])
+def test_device_resident_exchange_matches_one_island(world, team):
+    """pm_run_ga_islands_device -- the path the native NCCL exchange takes:
+    block records gathered device to device, the generation step (global best,
+    stop rule, migration) on the device -- gives the one-island RunResult for
+    2 and 4 islands, both migration modes, and both population draws."""
+    import threading
+
+    import paper_1610_10061_b200 as pm
+    from oracle.oracle import Oracle
+    o = Oracle()
+    costs = o.synth_euclid(300)
+    for pop in ("reference", "device"):
+        cfg = dict(nb=8, nt=32, evolve_limit=6, saturation=6, seed=9, population=pop, team=team)
+        with pm.Context(0) as ctx:
+            ctx.set_instance(costs, 300, 300, 30)
+            single = ctx.run_ga(pm.ga_config(**cfg))
+        fns = _device_ring(world)
+        out = [None] * world
+
+        def run(rank):
+            with pm.Context(0) as c:
+                c.set_instance(costs, 300, 300, 30)
+                out[rank] = c.run_ga(pm.ga_config(**cfg), rank=rank, world=world, allgather_device=fns[rank])
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(300)
+        for r in range(world):
+            got = out[r]
+            assert got is not None, r
+            assert got["best_cost"] == single["best_cost"] and (got["best"] == single["best"]).all()
+            assert got["kernels_executed"] == single["kernels_executed"]
+            assert got["kernel_of_best"] == single["kernel_of_best"]
+            assert (got["per_kernel_best_costs"] == single["per_kernel_best_costs"]).all()
