@@ -1,0 +1,22 @@
+#!/bin/bash
+# Round-2 measurement call: bench lines (ours syn20k/syn5k/pmed40/sweep, reference arm),
+# the ncu launch list of the default bench, full captures of K2 (syn20k), K2b (syn5k), K1 (syn20k),
+# stamped JSON records for bench.py's roofline.physical.
+set -u
+mkdir -p gpurun_out/r2
+O=gpurun_out/r2
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,driver_version --format=csv > $O/gpu.txt 2>&1
+lscpu > $O/lscpu.txt 2>&1
+timeout 900 python bench.py > $O/bench_syn20k.json 2> $O/bench_syn20k.err
+timeout 600 python bench.py --config syn5k --no-ga > $O/bench_syn5k.json 2> $O/bench_syn5k.err
+timeout 600 python bench.py --config pmed40 --no-ga > $O/bench_pmed40.json 2> $O/bench_pmed40.err
+timeout 600 python tools/sweep.py 5 > $O/p_sweep.md 2>&1
+timeout 900 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
+B="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-ga"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_syn20k.csv $B > $O/ncu_launch.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'^k_scan$' -c 1 -o $O/k2_scan_syn20k -f python tools/prof_eval.py syn20k scan 2 > $O/ncu_k2.log 2>&1
+python tools/ncu_to_json.py $O/k2_scan_syn20k.ncu-rep k_scan syn20k > $O/ncu_k2_json.log 2>&1; cp profiles/ncu_k_scan_syn20k.json $O/ 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'^k_gather' -c 1 -o $O/k2b_gather_syn5k -f python tools/prof_eval.py syn5k gather 2 > $O/ncu_k2b.log 2>&1
+python tools/ncu_to_json.py $O/k2b_gather_syn5k.ncu-rep k_gather syn5k > $O/ncu_k2b_json.log 2>&1; cp profiles/ncu_k_gather_syn5k.json $O/ 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'^k_(prep_costs|build_rows_cs)' -c 2 -o $O/k1_syn20k -f python tools/prof_eval.py syn20k scan 1 > $O/ncu_k1.log 2>&1
+for f in $O/*.json; do echo "== $f"; head -c 300 $f; echo; done
