@@ -40,7 +40,7 @@ def check_eval(ctx, n, m, p, costs, count, seed):
 
 
 def main():
-    which = sys.argv[1:] or ["eval", "wide", "k1", "ga", "orlib"]
+    which = sys.argv[1:] or ["eval", "wide", "k1", "prep", "walks", "ga", "orlib"]
     with pm.Context(0) as ctx:
         if "eval" in which:
             for n, m, p, count in ((5, 4, 2, 3), (130, 200, 20, 100), (300, 300, 30, 256), (600, 700, 7, 70)):
@@ -72,6 +72,31 @@ def main():
                 check_eval(ctx, 80, 120, 12, costs, 64, seed=6)
             os.environ.pop("PMB_K1")
             print("k1 ok", flush=True)
+        if "prep" in which:
+            # n * m > 2^20: the fused prep pass (u16 row copy with a padded
+            # stride when m % 8 != 0, u16 site-major table), both K1 paths
+            for n, m, p, mx in ((1100, 1100, 50, None), (1001, 1203, 40, 1000), (1030, 1030, 20, 70000)):
+                costs = o.synth_euclid(n) if mx is None else o.random_costs(n + 7, n, m, mx)
+                for k1 in ("count", "radix"):
+                    os.environ["PMB_K1"] = k1
+                    ctx.set_instance(costs, n, m, p)
+                    check_eval(ctx, n, m, p, costs, 96, seed=m)
+                os.environ.pop("PMB_K1")
+            print("prep ok", flush=True)
+        if "walks" in which:
+            import torch
+            n = m = 600
+            costs = o.synth_euclid(n)
+            ctx.set_instance(costs, n, m, 30)
+            pop = o.random_population(m, 30, 100, seed=4)
+            w = torch.from_numpy(pop.view(np.int64)).cuda()
+            gs = torch.zeros(4, dtype=torch.int64, device="cuda")
+            cm = torch.zeros(n, dtype=torch.int32, device="cuda")
+            ctx.scan_walks_device(w, gs, cm, 100, pop.shape[1])
+            so, inc = o.build_ordering(n, m, 30, costs)
+            _, _, _, sk = o.evaluate(so, inc, m, pop, want_sum_k=True)
+            assert int(gs.sum()) >= int(sk.max()) and int(cm.max()) <= m - 30 + 1
+            print("walks ok", flush=True)
         if "ga" in which:
             n = m = 200
             costs = o.synth_euclid(n)
