@@ -748,8 +748,15 @@ struct GVec {
   }
 };
 
+// Register budget (A/B switch): ptxas keeps 32 registers at the default
+// budget and issues the 8 client-vector loads as two halves; forcing 64 / 80 /
+// 94 registers (minimum 4 / 3 / 2 CTAs per SM) keeps all 8 in flight but loses
+// occupancy and measured slower at every shape (pmed40 0.213 -> 0.24-0.36 ms).
+#ifndef PMB_GATHER_MINB
+#define PMB_GATHER_MINB 0
+#endif
 template <class DistT, class OrdT>
-__global__ void __launch_bounds__(kGatherThreads)
+__global__ void __launch_bounds__(kGatherThreads, PMB_GATHER_MINB)
     k_gather(const DistT* __restrict__ dT, int nP, const OrdT* __restrict__ ord,
              const DistT* __restrict__ dist, int n, int m, int p, int W, int Wp,
              const uint64_t* __restrict__ words, int wp, const uint32_t* __restrict__ lists,
