@@ -467,14 +467,30 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
   PM_CUDA_TRY(c, cudaSetDevice(c->device));
   PM_CUDA_TRY(c, c->words.ensure(count * words_per * 8));
   PM_CUDA_TRY(c, c->costs_out.ensure(count * 8));
-  // chunks of whole 64-chromosome groups; small batches go in one piece
-  // Measured on B200: each extra launch costs a CTA-segment tail, which
-  // outweighs the overlap until a chunk carries >= 8192 chromosomes and
-  // >= 16 MB of words (the BASELINE batches stay in one piece).
+  // Chunks of whole 64-chromosome groups: the copy of chunk k+1 overlaps the
+  // kernels of chunk k, so only the first chunk's copy is exposed.  Each extra
+  // launch costs a CTA-segment tail (round 1: equal chunks only paid off from
+  // 8192 chromosomes and 16 MB on), so a batch of >= 4 MB is split into a short
+  // lead chunk (an eighth: its copy is the exposed part) and the rest;
+  // PMB_H2D_LEAD=0 sends it in one piece, PMB_H2D_LEAD=<d> leads with 1/d.
+  // Measured at syn20k, host-clock e2e (profiles/r02_e2e_ab.log): one piece
+  // 2.44 M evals/s, lead 1/8 2.47 M, 1/4 2.42 M, 1/2 2.35 M.
   const size_t bytes = count * words_per * 8;
-  const int chunks = (int)std::max<size_t>(
-      1, std::min<size_t>({(size_t)kErrSlots - 1, count / 8192, bytes / (16u << 20)}));
-  const size_t per = ((count + chunks - 1) / chunks + 63) / 64 * 64;
+  std::vector<size_t> starts{0};
+  {
+    const char* le = getenv("PMB_H2D_LEAD");
+    const size_t lead_div = le ? (size_t)std::atoll(le) : 8;
+    const int equal = (int)std::max<size_t>(
+        1, std::min<size_t>({(size_t)kErrSlots - 1, count / 8192, bytes / (16u << 20)}));
+    if (equal > 1) {
+      const size_t per = ((count + equal - 1) / equal + 63) / 64 * 64;
+      for (size_t off = per; off < count; off += per) starts.push_back(off);
+    } else if (lead_div >= 2 && bytes >= ((size_t)4 << 20) && count >= 256) {
+      const size_t lead = (count / lead_div + 63) / 64 * 64;
+      if (lead > 0 && lead < count) starts.push_back(lead);
+    }
+  }
+  const int chunks = (int)starts.size();
   while ((int)c->chunk_ev.size() < chunks) {
     cudaEvent_t e;
     PM_CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -489,8 +505,9 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
   PM_CUDA_TRY(c, cudaEventRecord(c->entry_ev, c->stream));
   PM_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->entry_ev, 0));
   int used = 0;
-  for (size_t off = 0; off < count; off += per, ++used) {
-    const size_t cnt = std::min(per, count - off);
+  for (; used < chunks; ++used) {
+    const size_t off = starts[used];
+    const size_t cnt = (used + 1 < chunks ? starts[used + 1] : count) - off;
     PM_CUDA_TRY(c, cudaMemcpyAsync(c->words.as<uint64_t>() + off * words_per, bitsets + off * words_per,
                                    cnt * words_per * 8, cudaMemcpyHostToDevice, c->copy_stream));
     PM_CUDA_TRY(c, cudaEventRecord(c->chunk_ev[used], c->copy_stream));
@@ -505,7 +522,7 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   for (int i = 0; i < used; ++i)
     if (errs[i] != ~0ull) {
-      if (first_bad) *first_bad = (size_t)i * per + (size_t)errs[i];
+      if (first_bad) *first_bad = starts[i] + (size_t)errs[i];
       return c->fail(PM_CONTRACT, mode == 1 ? kMsgNoneOpen : kMsgRunoff);
     }
   return PM_OK;
