@@ -224,6 +224,17 @@ def test_pipelined_host_call_reports_global_first_bad(ctx, pm, oracle):
     with pytest.raises(pm.ContractError) as ei:
         ctx.evaluate(bad)
     assert ei.value.first_bad == 12001
+    # a 4096 batch (10 MB) goes as a lead chunk of 512 and the rest
+    small = pop[:4096].copy()
+    assert (ctx.evaluate(small) == good[:4096]).all()
+    small[3000] = 0
+    with pytest.raises(pm.ContractError) as ei:
+        ctx.evaluate(small)
+    assert ei.value.first_bad == 3000
+    small[100] = 0
+    with pytest.raises(pm.ContractError) as ei:
+        ctx.evaluate(small)
+    assert ei.value.first_bad == 100
 
 
 def test_counting_sort_path_and_handback(ctx, oracle):
