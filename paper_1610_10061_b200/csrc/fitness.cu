@@ -115,6 +115,12 @@ constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
 #ifndef PMB_X_RED
 #define PMB_X_RED 0
 #endif
+// ... and for the short-segment shapes of the many-warp variant only (2- and
+// 4-warp CTAs: pmed40-size instances, the GA's evaluation batches), where the
+// split records and the FLO-indexed drain measured faster (0.072 -> 0.069 ms)
+#ifndef PMB_X_SHORT
+#define PMB_X_SHORT 1
+#endif
 constexpr int kWideWarps = 24, kWideQueue = 256;  // the many-warp K2 variant (plan_scan)
 #ifndef PMB_QCHECK
 #define PMB_QCHECK 2
@@ -169,14 +175,12 @@ struct Chunk {
 template <class MaskT>
 struct MaskOps {
   static constexpr int kG = 8 * sizeof(MaskT);
+  template <bool kFlo>
   __device__ __forceinline__ static int pop_high(MaskT& h) {  // index of the top set bit, cleared
     if constexpr (sizeof(MaskT) == 4) {
-#if PMB_X_BFIND
       int c;
-      asm("bfind.u32 %0, %1;" : "=r"(c) : "r"(h));  // FLO: the top bit's position directly
-#else
-      const int c = 31 - __clz(h);
-#endif
+      if constexpr (kFlo) asm("bfind.u32 %0, %1;" : "=r"(c) : "r"(h));  // FLO: the top bit's position directly
+      else c = 31 - __clz(h);
       h ^= 1u << c;
       return c;
     } else {
@@ -235,12 +239,15 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
   constexpr bool kPacked = sizeof(MaskT) == 4 && sizeof(AccT) == 4;
   MaskT* wqh = kPacked ? hbuf + (size_t)warp * 2 * kQ : hbuf + (size_t)warp * kQ;
   AccT* wqd = kPacked ? reinterpret_cast<AccT*>(wqh + kQ) : dbuf + (size_t)warp * kQ;
-  uint64_t* wq = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kQ;  // one 8-byte record (!PMB_X_SPLITQ)
+  uint64_t* wq = reinterpret_cast<uint64_t*>(hbuf) + (size_t)warp * kQ;  // one 8-byte record (!kSplitQ)
   (void)wq;
   // u16 sorted distances: a record of an even column stores the raw 32-bit
   // word holding the column's cost in its low half (no extraction in the
   // column loop); the drain masks it
-  constexpr bool kRawCost = PMB_X_SPLITQ && !kDepth && sizeof(DistT) == 2 && sizeof(AccT) == 4;
+  constexpr bool kShortCta = kW > 0 && kCtaW < kW;
+  constexpr bool kSplitQ = kPacked && (PMB_X_SPLITQ || (PMB_X_SHORT && kShortCta));
+  constexpr bool kFlo = PMB_X_BFIND || (PMB_X_SHORT && kShortCta);
+  constexpr bool kRawCost = kSplitQ && !kDepth && sizeof(DistT) == 2 && sizeof(AccT) == 4;
 
   const long long U = (long long)groups * n;
   long long u = U * blockIdx.x / gridDim.x;
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
           MaskT h = 0;
           AccT dv = 0;
           if (base + lane < qn) {
-            if constexpr (kPacked && !PMB_X_SPLITQ) {
+            if constexpr (kPacked && !kSplitQ) {
               const uint64_t x = wq[base + lane];
               h = (MaskT)x;
               dv = (AccT)(x >> 32);
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
             if constexpr (kRawCost) dv &= 0xffffu;
           }
           while (h) {
-            const int c = Ops::pop_high(h);
+            const int c = Ops::template pop_high<kFlo>(h);
 #if PMB_X_RED
             // a shared-memory reduction: lane-private column (no contention),
             // and the lane does not wait for a load-add-store round trip
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
           else dval = (AccT)cur.cost(j);
           const uint32_t q = qn + __popc(hb & lt);
           PMB_CHECK(q < (uint32_t)kQ);
-          if constexpr (kPacked && !PMB_X_SPLITQ) {
+          if constexpr (kPacked && !kSplitQ) {
             wq[q] = (uint64_t)h | ((uint64_t)dval << 32);
           } else {
             wqh[q] = h;
