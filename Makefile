@@ -18,6 +18,12 @@ build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) includ
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -Xptxas -warn-spills -c $< -o $@
 
+# the scan (K2) schedules better with ptxas's aggressive register heuristics
+# (syn20k 1.433 -> 1.415 ms, profiles/r02_k2_ab.md); the gather (gather.cu)
+# does not (it loses occupancy), hence separate translation units
+build/fitness.o: NVFLAGS += -Xptxas --register-usage-level=10
+build_bounds/fitness.o: NVFLAGS += -Xptxas --register-usage-level=10
+
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart_static -lrt -ldl -lpthread
 

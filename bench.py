@@ -209,7 +209,8 @@ def ncu_record(config: str, kernel: str):
         return None
     with open(path) as f:
         rec = json.load(f)
-    rec["stale"] = rec.get("source_sha16") != source_hash("paper_1610_10061_b200/csrc/fitness.cu")
+    src = rec.get("source_file", "paper_1610_10061_b200/csrc/fitness.cu")
+    rec["stale"] = rec.get("source_sha16") != source_hash(src)
     rec["file"] = os.path.relpath(path, ROOT)
     return rec
 
@@ -413,7 +414,8 @@ def run_ours(args):
                                                          "sm_throughput_pct", "lts_throughput_pct",
                                                          "dram_throughput_pct", "warp_instructions",
                                                          "duration_ms")}
-        physical["ncu_source"] = {k: ncu.get(k) for k in ("file", "source_sha16", "stale", "commit", "captured")}
+        physical["ncu_source"] = {k: ncu.get(k) for k in ("file", "source_file", "source_sha16", "stale", "commit",
+                                                           "captured")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

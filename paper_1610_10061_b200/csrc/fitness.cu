@@ -17,12 +17,12 @@
 // are accumulated into per-lane private shared-memory counters (no atomics) and
 // reduced once per CTA segment.
 //
-// K2b ("gather", gather-min).  fitness = sum_i min_{j open} cost(i, j)
+// K2b ("gather", gather-min, gather.cu).  fitness = sum_i min_{j open} cost(i, j)
 // (instance.cpp:32-48, equal to the scan by acceptance.cpp:86-116).  A thread
 // owns 16 bytes of consecutive clients (8 at u16 costs); each open site j of a
 // chromosome is one 16-byte read of the site-major row dT[j][i0..] and a packed
 // min.  Wins when p is small (the scan reads ~m/p columns per client, the
-// gather p): AUTO picks the scan iff p >= 1.05 sqrt(m), measured.  The reference's scan-width contract
+// gather p): AUTO picks the scan iff p >= 1.01 sqrt(m), measured.  The reference's scan-width contract
 // (ordering.cpp:50-52) is enforced exactly: with popcount >= p it cannot fail
 // (W = m-p+1 columns always contain one of p distinct sites); with fewer open
 // sites the (cost, site)-smallest open site must not sort after column W-1.
@@ -680,240 +680,6 @@ cudaError_t launch_walks(const DevTables& t, const uint64_t* T, size_t count, un
     k_walks<uint32_t><<<blocks, 256, 0, st>>>((const uint32_t*)t.ord, t.n, t.W, t.Wp, T, scan_t_stride(t.m),
                                                count, group_sum, client_max);
   return cudaGetLastError();
-}
-
-// ---- K2b: gather-min -----------------------------------------------------------
-
-// One warp per chromosome: compact the open sites (< m) into a list.
-__global__ void __launch_bounds__(256) k_open_lists(const uint64_t* __restrict__ words, size_t count,
-                                                    int wp, int m, uint32_t* __restrict__ lists,
-                                                    uint32_t* __restrict__ counts, int cap,
-                                                    unsigned long long* __restrict__ costs) {
-  const size_t c = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (c >= count) return;
-  const int lane = threadIdx.x & 31;
-  if (lane == 0) costs[c] = 0;  // the gather accumulates into costs (replaces a memset launch)
-  const unsigned lt = lanemask_lt();
-  const uint64_t* w = words + c * wp;
-  uint32_t* list = lists + c * (size_t)cap;
-  uint32_t total = 0;
-  for (int w0 = 0; w0 < wp; w0 += 32) {
-    const int wi = w0 + lane;
-    uint64_t x = wi < wp ? w[wi] : 0;
-    if (wi == wp - 1 && (m & 63)) x &= (1ull << (m & 63)) - 1;  // bits >= m are not sites
-    const uint32_t pc = __popcll(x);
-    uint32_t incl = pc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += t;
-    }
-    uint32_t pos = total + incl - pc;
-    while (x) {
-      const int b = __ffsll((long long)x) - 1;
-      x &= x - 1;
-      if (pos < (uint32_t)cap) list[pos] = (uint32_t)(wi * 64 + b);
-      ++pos;
-    }
-    total += __shfl_sync(kFull, incl, 31);
-    (void)lt;
-  }
-  if (lane == 0) counts[c] = total;
-}
-
-constexpr int kGatherThreads = 256;
-
-// V consecutive clients per thread through one 16-byte load per open site.
-template <class DistT>
-struct GVec {
-  static constexpr int V = 16 / sizeof(DistT);
-  uint4 v;
-  __device__ __forceinline__ void set_max() { v = make_uint4(~0u, ~0u, ~0u, ~0u); }
-  __device__ __forceinline__ void min_with(const uint4 o) {
-    if constexpr (sizeof(DistT) == 2) {
-      v.x = __vminu2(v.x, o.x);
-      v.y = __vminu2(v.y, o.y);
-      v.z = __vminu2(v.z, o.z);
-      v.w = __vminu2(v.w, o.w);
-    } else if constexpr (sizeof(DistT) == 4) {
-      v.x = min(v.x, o.x);
-      v.y = min(v.y, o.y);
-      v.z = min(v.z, o.z);
-      v.w = min(v.w, o.w);
-    } else {
-      const uint64_t a0 = (uint64_t)v.x | ((uint64_t)v.y << 32), b0 = (uint64_t)o.x | ((uint64_t)o.y << 32);
-      const uint64_t a1 = (uint64_t)v.z | ((uint64_t)v.w << 32), b1 = (uint64_t)o.z | ((uint64_t)o.w << 32);
-      const uint64_t m0 = a0 < b0 ? a0 : b0, m1 = a1 < b1 ? a1 : b1;
-      v = make_uint4((uint32_t)m0, (uint32_t)(m0 >> 32), (uint32_t)m1, (uint32_t)(m1 >> 32));
-    }
-  }
-  __device__ __forceinline__ uint64_t elem(int q) const {
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(&v);
-    if constexpr (sizeof(DistT) == 2) return (w[q >> 1] >> ((q & 1) * 16)) & 0xffffu;
-    else if constexpr (sizeof(DistT) == 4) return w[q];
-    else return (uint64_t)w[2 * q] | ((uint64_t)w[2 * q + 1] << 32);
-  }
-};
-
-// Register budget (A/B switch): ptxas keeps 32 registers at the default
-// budget and issues the 8 client-vector loads as two halves; forcing 64 / 80 /
-// 94 registers (minimum 4 / 3 / 2 CTAs per SM) keeps all 8 in flight but loses
-// occupancy and measured slower at every shape (pmed40 0.213 -> 0.24-0.36 ms).
-#ifndef PMB_GATHER_MINB
-#define PMB_GATHER_MINB 0
-#endif
-template <class DistT, class OrdT>
-__global__ void __launch_bounds__(kGatherThreads, PMB_GATHER_MINB)
-    k_gather(const DistT* __restrict__ dT, int nP, const OrdT* __restrict__ ord,
-             const DistT* __restrict__ dist, int n, int m, int p, int W, int Wp,
-             const uint64_t* __restrict__ words, int wp, const uint32_t* __restrict__ lists,
-             const uint32_t* __restrict__ counts, int cap, size_t count, int chunk,
-             unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err, int mode) {
-  using Vec = GVec<DistT>;
-  constexpr int V = Vec::V;
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* part = reinterpret_cast<unsigned long long*>(smem);  // [warps][chunk]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kWarps = kGatherThreads / 32;
-  const int i0 = (blockIdx.x * kGatherThreads + tid) * V;  // first client of this thread
-  const int nv = i0 < n ? min(V, n - i0) : 0;               // real clients among the V
-  const DistT* col = dT + i0;
-  // chromosome chunks stride over gridDim.y (<= 65535): any population size launches
-  for (size_t cbase = (size_t)blockIdx.y * chunk; cbase < count; cbase += (size_t)gridDim.y * chunk) {
-  const int cn = (int)min((size_t)chunk, count - cbase);
-  for (int cl = 0; cl < cn; ++cl) {
-    const size_t c = cbase + cl;
-    const uint32_t pc = counts[c];
-    unsigned long long sum = 0;
-    if (pc == 0) {
-      if (tid == 0 && blockIdx.x == 0) atomicMin(err, (unsigned long long)c);
-    } else if (pc <= (uint32_t)cap && !(mode == 0 && pc < (uint32_t)p)) {
-      // common case: min over the open list, V clients per 16-byte load
-      Vec best;
-      best.set_max();
-      if (nv > 0) {
-        const uint32_t* list = lists + c * (size_t)cap;
-        uint32_t t = 0;
-        PMB_CHECK(i0 + V <= nP && pc <= (uint32_t)cap);
-        // 8 open sites per step: their indices arrive as two 16-byte loads
-        // (lists are 16-byte aligned, cap % 4 == 0) and the 8 client-vector
-        // loads are all in flight before the first min (the kernel is bound by
-        // L2 latency, not bandwidth)
-        for (; t + 8 <= pc; t += 8) {
-          const uint4 ja = __ldg(reinterpret_cast<const uint4*>(list + t));
-          const uint4 jb = __ldg(reinterpret_cast<const uint4*>(list + t + 4));
-          const uint32_t js[8] = {ja.x, ja.y, ja.z, ja.w, jb.x, jb.y, jb.z, jb.w};
-          uint4 x[8];
-#ifdef PMB_BOUNDS
-          for (int u = 0; u < 8; ++u) PMB_CHECK(js[u] < (uint32_t)m);
-#endif
-#pragma unroll
-          for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)js[u] * nP));
-#pragma unroll
-          for (int u = 0; u < 8; ++u) best.min_with(x[u]);
-        }
-        if (t + 4 <= pc) {
-          const uint4 ja = __ldg(reinterpret_cast<const uint4*>(list + t));
-          const uint32_t js[4] = {ja.x, ja.y, ja.z, ja.w};
-          uint4 x[4];
-#ifdef PMB_BOUNDS
-          for (int u = 0; u < 4; ++u) PMB_CHECK(js[u] < (uint32_t)m);
-#endif
-#pragma unroll
-          for (int u = 0; u < 4; ++u) x[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)js[u] * nP));
-#pragma unroll
-          for (int u = 0; u < 4; ++u) best.min_with(x[u]);
-          t += 4;
-        }
-        for (; t < pc; ++t) best.min_with(__ldg(reinterpret_cast<const uint4*>(col + (size_t)__ldg(list + t) * nP)));
-#pragma unroll
-        for (int q = 0; q < V; ++q)
-          if (q < nv) sum += best.elem(q);
-      }
-    } else {
-      // general path: walk the words in site order, track the (cost, site)
-      // minimum per client and, under the fitness contract with fewer than p
-      // open sites, check it sorts within the first W columns (ordering.cpp:50-52).
-      bool bad = false;
-      for (int q = 0; q < nv; ++q) {
-        const int i = i0 + q;
-        uint64_t best = ~0ull;
-        uint32_t bj = 0;
-        const uint64_t* w = words + c * wp;
-        for (int wi = 0; wi < wp; ++wi) {
-          uint64_t x = __ldg(w + wi);
-          if (wi == wp - 1 && (m & 63)) x &= (1ull << (m & 63)) - 1;
-          while (x) {
-            const uint32_t j = wi * 64 + (__ffsll((long long)x) - 1);
-            x &= x - 1;
-            const uint64_t v = (uint64_t)dT[(size_t)j * nP + i];
-            if (v < best) {  // strict: ascending j keeps the lowest site on ties
-              best = v;
-              bj = j;
-            }
-          }
-        }
-        sum += best;
-        if (mode == 0 && pc < (uint32_t)p) {
-          const uint64_t dlast = (uint64_t)dist[(size_t)i * Wp + (W - 1)];
-          const uint32_t jlast = (uint32_t)ord[(size_t)i * Wp + (W - 1)];
-          bad |= !(best < dlast || (best == dlast && bj <= jlast));
-        }
-      }
-      if (__any_sync(kFull, bad) && lane == 0) atomicMin(err, (unsigned long long)c);
-    }
-    sum = warp_sum(sum);
-    if (lane == 0) part[warp * chunk + cl] = sum;
-  }
-  __syncthreads();
-  for (int cl = tid; cl < cn; cl += kGatherThreads) {
-    unsigned long long s = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += part[w * chunk + cl];
-    atomicAdd(&costs[cbase + cl], s);
-  }
-  __syncthreads();  // `part` is rewritten by the next chunk
-  }
-}
-
-template <class DistT, class OrdT>
-static cudaError_t launch_gather_t(const DevTables& t, const uint64_t* words, size_t count, int wp,
-                                   const uint32_t* lists, const uint32_t* counts, int cap,
-                                   unsigned long long* costs, unsigned long long* err, int mode,
-                                   int sms, cudaStream_t st) {
-  constexpr int V = 16 / sizeof(DistT);
-  const int xblocks = (t.n + kGatherThreads * V - 1) / (kGatherThreads * V);
-  // enough CTAs for ~8 resident CTAs per SM
-  const long long want = (long long)sms * 8;
-  const int chunk = (int)std::max<long long>(1, std::min<long long>(256, (long long)count * xblocks / want));
-  const unsigned yblocks = (unsigned)std::min<size_t>((count + chunk - 1) / chunk, 65535);
-  const size_t smem = (size_t)(kGatherThreads / 32) * chunk * 8;
-  k_gather<DistT, OrdT><<<dim3(xblocks, yblocks), kGatherThreads, smem, st>>>(
-      (const DistT*)t.dT, t.nP, (const OrdT*)t.ord, (const DistT*)t.dist, t.n, t.m, t.p, t.W, t.Wp, words,
-      wp, lists, counts, cap, count, chunk, costs, err, mode);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_open_lists(const uint64_t* words, size_t count, int words_per, int m,
-                              uint32_t* open_lists, uint32_t* open_counts, int open_cap,
-                              unsigned long long* costs, cudaStream_t st) {
-  k_open_lists<<<(unsigned)((count + 7) / 8), 256, 0, st>>>(words, count, words_per, m, open_lists,
-                                                             open_counts, open_cap, costs);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gather(const DevTables& t, const uint64_t* words, size_t count, int words_per,
-                          uint32_t* open_lists, uint32_t* open_counts, int open_cap,
-                          unsigned long long* costs_acc, unsigned long long* err_first_bad, int mode,
-                          int sms, cudaStream_t st) {
-  if (t.site_bytes == 2) {
-    if (t.dist_bytes == 2) return launch_gather_t<uint16_t, uint16_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
-    if (t.dist_bytes == 4) return launch_gather_t<uint32_t, uint16_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
-    return launch_gather_t<uint64_t, uint16_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
-  }
-  if (t.dist_bytes == 2) return launch_gather_t<uint16_t, uint32_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
-  if (t.dist_bytes == 4) return launch_gather_t<uint32_t, uint32_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
-  return launch_gather_t<uint64_t, uint32_t>(t, words, count, words_per, open_lists, open_counts, open_cap, costs_acc, err_first_bad, mode, sms, st);
 }
 
 }  // namespace pmb

@@ -8,7 +8,7 @@ mkdir -p build_ab
 git show "$rev":paper_1610_10061_b200/csrc/fitness.cu > paper_1610_10061_b200/csrc/fitness_ab.cu
 trap 'rm -f paper_1610_10061_b200/csrc/fitness_ab.cu' EXIT
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr"
-nvcc $F -c paper_1610_10061_b200/csrc/fitness_ab.cu -o build_ab/fitness.o
+nvcc $F -Xptxas --register-usage-level=10 -c paper_1610_10061_b200/csrc/fitness_ab.cu -o build_ab/fitness.o
 others=$(ls build/*.o | grep -v '/fitness.o$')
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_1610_10061_b200/libpmedian_b200_ab.so \
   $others build_ab/fitness.o -lcudart_static -lrt -ldl -lpthread

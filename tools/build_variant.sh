@@ -7,7 +7,7 @@ set -e
 name=$1; flags=$2
 mkdir -p build_var/$name
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr"
-nvcc $F $flags -c paper_1610_10061_b200/csrc/fitness.cu -o build_var/$name/fitness.o
+nvcc $F -Xptxas --register-usage-level=10 $flags -c paper_1610_10061_b200/csrc/fitness.cu -o build_var/$name/fitness.o
 others=$(ls build/*.o | grep -v '/fitness.o$')
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_1610_10061_b200/libpmedian_b200_$name.so \
   $others build_var/$name/fitness.o -lcudart_static -lrt -ldl -lpthread

@@ -3,9 +3,9 @@ bench.py reads (profiles/ncu_<kernel>_<config>.json):
 
     python tools/ncu_to_json.py <report.ncu-rep> <kernel> <config> [commit]
 
-The record carries the SHA-256 (16 hex) of the kernel source the capture ran,
-so bench.py reports it as `stale` once paper_1610_10061_b200/csrc/fitness.cu
-changes.  Run it next to the capture (on the GPU box, the snapshot's source)."""
+The record carries the SHA-256 (16 hex) of the kernel's source file the capture
+ran (csrc/fitness.cu for k_scan, csrc/gather.cu for k_gather), so bench.py
+reports it as `stale` once that file changes.  Run it next to the capture (on the GPU box, the snapshot's source)."""
 import csv
 import hashlib
 import io
@@ -17,6 +17,8 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 _T = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
+KERNEL_SOURCE = {"k_scan": "fitness.cu", "k_gather": "gather.cu", "k_build_rows_cs": "ordering.cu",
+                 "k_prep_costs": "ordering.cu"}
 _B = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
@@ -45,7 +47,8 @@ def main():
         return None if v is None else v * _B.get(u[key], 1)
 
     rd, wr = bytes_("dram__bytes_read.sum"), bytes_("dram__bytes_write.sum")
-    with open(os.path.join(ROOT, "paper_1610_10061_b200/csrc/fitness.cu"), "rb") as f:
+    src = KERNEL_SOURCE.get(kernel, "fitness.cu")
+    with open(os.path.join(ROOT, "paper_1610_10061_b200/csrc", src), "rb") as f:
         sha = hashlib.sha256(f.read()).hexdigest()[:16]
     rec = {
         "kernel": kernel, "config": config, "report": os.path.basename(rep),
@@ -63,7 +66,7 @@ def main():
         "shared_st_bank_conflicts": num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum"),
         "occupancy_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
         "registers": num("launch__registers_per_thread"),
-        "source_sha16": sha, "commit": commit,
+        "source_file": "paper_1610_10061_b200/csrc/" + src, "source_sha16": sha, "commit": commit,
         "captured": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
         "how": "ncu --set full --clock-control none --import-source on (one launch, cold L2, serialised)",
     }
