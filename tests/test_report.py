@@ -69,3 +69,28 @@ def test_reference_combinatorics_unit_tests_on_the_compat_headers(tmp_path):
                     os.path.join(ROOT, "tests", "cpp", "ref_tests_main.cpp"), src, "-o", exe], check=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "9 test cases, 0 failed checks" in r.stdout, r.stdout + r.stderr
+
+
+def test_compat_random_chromosome_equals_the_reference(tmp_path, reflib):
+    """The compat host draw (BigInt binomial, rejection draw, unranking)
+    consumes the keyed stream exactly as the reference's random_chromosome
+    (combinatorics.cpp:54-75): identical chromosomes, including multi-word
+    ranks (C(300, 40) ~ 2^163) and the paper's shapes."""
+    import numpy as np
+    exe = str(tmp_path / "draw")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include", "compat"), "-I",
+                    os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "cpp", "test_compat_draw.cpp"),
+                    "-o", exe], check=True)
+    cases = [(4, 2, 7, 50), (100, 5, 1, 40), (300, 40, 9, 20), (900, 90, 3, 8), (65, 64, 2, 5)]
+    r = subprocess.run([exe], input="".join(f"{m} {p} {s} {c}\n" for m, p, s, c in cases), capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    at = 0
+    for m, p, seed, count in cases:
+        wp = (m + 63) // 64
+        want = np.zeros(count * wp, dtype=np.uint64)
+        assert reflib.L.ref_random_chromosome(m, p, seed, count, want) == 0
+        got = np.array([[int(x) for x in ln.split()] for ln in lines[at:at + count]], dtype=np.uint64).reshape(-1)
+        at += count
+        assert (got == want).all(), (m, p, seed)
