@@ -163,6 +163,15 @@ def allgather_into(dst, src):
     dst.copy_(torch.cat(parts))
 
 
+def shard(count: int, world: int, rank: int):
+    """The strong split (BASELINE configs 3-4): rank r evaluates the contiguous
+    chromosomes [r * count / world, (r + 1) * count / world) of the one batch."""
+    if count % world:
+        raise ValueError(f"strong scaling needs the population ({count}) divisible by {world}")
+    per = count // world
+    return rank * per, (rank + 1) * per
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -296,8 +305,9 @@ def run_ours(args):
     # all-gathered back; weak: every rank its own population of `count`
     if scaling == "strong":
         pop_all = synth.random_population(m, p, count, seed=7)
-        per = count // world
-        pop = pop_all[rank * per:(rank + 1) * per]
+        lo, hi = shard(count, world, rank)
+        per = hi - lo
+        pop = pop_all[lo:hi]
     else:
         pop_all = None
         per = count
