@@ -46,6 +46,8 @@ SHAPES = [("pmed40", 900, 90, 15360), ("syn5k", 5000, 50, 1024), ("syn20k", 2000
 GA_RUNS = {  # name: (npts, p, nb, nt, evolve_limit, saturation, seed)
     "table1_pmed40_shape": (900, 90, 60, 256, 100, 10, 1),
     "syn20k_islands_2gen": (20000, 200, 16, 256, 2, 3, 1),
+    # the run bench.py times for the syn20k island GA figure (evolve_limit 20, saturation 21)
+    "syn20k_islands_20gen": (20000, 200, 16, 256, 20, 21, 1),
 }
 
 

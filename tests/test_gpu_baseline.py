@@ -111,6 +111,19 @@ def test_syn20k_island_ga_matches_reference_run_ga(ctx, pm, golden):
     assert _runresult(ctx.run_ga(cfg)) == _want(gr)
 
 
+def test_syn20k_island_ga_bench_run_matches_reference(ctx, pm, golden):
+    """The exact run behind bench.py's syn20k island-GA gens/s figure (nb=16,
+    nt=256, evolve_limit 20, saturation 21, seed 1): all 20 generations equal
+    the reference run_ga (which takes ~50 minutes on 8 host threads)."""
+    gr = golden[0]["ga"].get("syn20k_islands_20gen")
+    if gr is None:
+        pytest.skip("golden not generated")
+    _instance(ctx, gr["n"], gr["p"])
+    cfg = pm.ga_config(nb=gr["nb"], nt=gr["nt"], evolve_limit=gr["evolve_limit"], saturation=gr["saturation"],
+                       seed=gr["seed"])
+    assert _runresult(ctx.run_ga(cfg)) == _want(gr)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
