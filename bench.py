@@ -521,14 +521,20 @@ def bench_ga(ctx, args, world, rank, local, n, m, p):
                            population=pop_mode)
         warm = pm.ga_config(nb=nb, nt=256, evolve_limit=1, saturation=1, seed=2, population=pop_mode)
         ctx.run_ga(warm, rank=rank, world=world, allgather=ag)  # kernels loaded, Pascal table resident
+        ctx.profile_read()
+        ctx.set_profiling(True)  # CUDA events around every fitness-kernel launch of the run
         r = ctx.run_ga(cfg, rank=rank, world=world, allgather=ag)
+        ctx.set_profiling(False)
+        eval_ms, eval_launches = ctx.profile_read()
         out[key] = {"config": f"n=m={n}, p={p}, nb={nb} ({nb // world} per GPU), nt=256, {pop_mode} population draw",
                     "gens_per_s": r["kernels_executed"] / r["wall_time"], "generations": r["kernels_executed"],
+                    "fitness_kernel_share_of_wall": eval_ms / 1e3 / r["wall_time"],
+                    "fitness_kernel_launches": eval_launches,
                     "best_cost": r["best_cost"], "evals_per_gen_reference_semantics":
                         r["evaluations"] / r["kernels_executed"],
                     "device_evals_per_gen": r["device_evaluations"] / r["kernels_executed"],
                     "exchange": "none (1 island)" if world == 1 else (
-                        "pm_nccl_allgather (library NCCL communicator)" if BACKEND == "nccl"
+                        "pm_nccl_allgather_device (library NCCL communicator, device buffers)" if BACKEND == "nccl"
                         else "torch.distributed gloo allgather")}
     if isinstance(ag, pm.NcclComm):
         ag.close()
