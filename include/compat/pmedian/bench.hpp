@@ -158,6 +158,8 @@ inline std::string json_string(std::string_view s) {
       case '\n': o += "\\n"; break;
       case '\t': o += "\\t"; break;
       case '\r': o += "\\r"; break;
+      case '\b': o += "\\b"; break;
+      case '\f': o += "\\f"; break;
       default:
         if (static_cast<unsigned char>(ch) < 0x20) {
           char b[8];
@@ -200,13 +202,35 @@ struct JsonLine {
             case 'r': ch = '\r'; break;
             case 'b': ch = '\b'; break;
             case 'f': ch = '\f'; break;
-            case 'u': {
-              if (i + 4 > s.size()) fail("bad escape");
-              unsigned v = 0;
-              std::from_chars(s.data() + i, s.data() + i + 4, v, 16);
-              i += 4;
-              ch = static_cast<char>(v);
-              break;
+            case 'u': {  // \uXXXX (a surrogate pair for code points above U+FFFF), written as UTF-8
+              auto hex4 = [&]() -> unsigned {
+                unsigned v = 0;
+                if (i + 4 > s.size() || std::from_chars(s.data() + i, s.data() + i + 4, v, 16).ptr != s.data() + i + 4)
+                  fail("bad \\u escape");
+                i += 4;
+                return v;
+              };
+              unsigned cp = hex4();
+              if (cp >= 0xD800 && cp < 0xDC00 && i + 6 <= s.size() && s[i] == '\\' && s[i + 1] == 'u') {
+                i += 2;
+                cp = 0x10000 + ((cp - 0xD800) << 10) + (hex4() - 0xDC00);
+              }
+              if (cp < 0x80) {
+                out += static_cast<char>(cp);
+              } else if (cp < 0x800) {
+                out += static_cast<char>(0xC0 | (cp >> 6));
+                out += static_cast<char>(0x80 | (cp & 0x3F));
+              } else if (cp < 0x10000) {
+                out += static_cast<char>(0xE0 | (cp >> 12));
+                out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+                out += static_cast<char>(0x80 | (cp & 0x3F));
+              } else {
+                out += static_cast<char>(0xF0 | (cp >> 18));
+                out += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
+                out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+                out += static_cast<char>(0x80 | (cp & 0x3F));
+              }
+              continue;
             }
             default: ch = e;
           }

@@ -52,7 +52,14 @@ class ContextPool {
     }
     return std::make_unique<b200::Tables>(device);
   }
+  // Only contexts holding small instances are kept: a pooled context keeps its
+  // device tables, so a large one (gigabytes at n = m = 20000) is destroyed
+  // rather than parked.
   void give(int device, std::unique_ptr<b200::Tables> t) {
+    pm_table_info ti{};
+    if (pm_table_info_get(t->handle(), &ti) == PM_OK &&
+        ti.clients * ti.row_stride * (std::size_t)(ti.site_bytes + 2 * ti.dist_bytes) > ((std::size_t)64 << 20))
+      return;  // `t` is destroyed here
     std::lock_guard<std::mutex> lock(mu_);
     if (free_.size() < 8) free_.emplace_back(device, std::move(t));
   }
