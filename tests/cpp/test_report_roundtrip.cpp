@@ -49,7 +49,7 @@ static std::vector<BenchmarkRecord> records() {
   c.search_space = pmedian::binomial(20000, 200);
   v.push_back(c);
   BenchmarkRecord d = b;
-  d.instance_code = "zero";
+  d.instance_code = "zero\ttab\bbs\fff\x01ctl\u00e9";
   d.best_cost = 0;
   d.reference_cost = 0;
   d.approximation_ratio = 1.0;
