@@ -99,6 +99,7 @@ class ClockSampler:
                     time.sleep(0.002)
 
             self._sample = sample
+            sample()  # the region's start, even when it is shorter than a tick
 
             self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
