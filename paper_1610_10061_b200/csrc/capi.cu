@@ -83,6 +83,7 @@ void pm_destroy(pm_ctx* c) {
   c->ga.hrec.release();
   c->ga.hglob.release();
   c->ga.hflag.release();
+  c->hout.release();
   for (auto* v : {&c->ev_used, &c->ev_free})
     for (auto& e : *v) {
       cudaEventDestroy(e.first);
@@ -382,7 +383,8 @@ int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcos
     const size_t groups = (count + 63) / 64;
     PM_CUDA_TRY(c, c->T.ensure(groups * scan_t_stride(t.m) * 8));
     PM_CUDA_TRY(c, launch_transpose_population(dwords, count, wp, t.m, c->T.as<uint64_t>(),
-                                               reinterpret_cast<unsigned long long*>(dcosts), c->stream));
+                                               reinterpret_cast<unsigned long long*>(dcosts), errw_override,
+                                               c->stream));
     if (c->profiling) {
       ev = c->ev_get();
       cudaEventRecord(ev.first, c->stream);
@@ -394,7 +396,7 @@ int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcos
     PM_CUDA_TRY(c, c->counts.ensure(count * 4));
     PM_CUDA_TRY(c, launch_open_lists(dwords, count, wp, t.m, c->lists.as<uint32_t>(),
                                      c->counts.as<uint32_t>(), c->open_cap,
-                                     reinterpret_cast<unsigned long long*>(dcosts), c->stream));
+                                     reinterpret_cast<unsigned long long*>(dcosts), errw_override, c->stream));
     if (c->profiling) {
       ev = c->ev_get();
       cudaEventRecord(ev.first, c->stream);
@@ -466,7 +468,9 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
   if (count == 0) return PM_OK;
   PM_CUDA_TRY(c, cudaSetDevice(c->device));
   PM_CUDA_TRY(c, c->words.ensure(count * words_per * 8));
-  PM_CUDA_TRY(c, c->costs_out.ensure(count * 8));
+  // costs followed by the per-chunk error words: one device-to-host copy into pinned staging
+  PM_CUDA_TRY(c, c->costs_out.ensure((count + kErrSlots) * 8));
+  PM_CUDA_TRY(c, c->hout.ensure((count + kErrSlots) * 8));
   // Chunks of whole 64-chromosome groups: the copy of chunk k+1 overlaps the
   // kernels of chunk k, so only the first chunk's copy is exposed.  Each extra
   // launch costs a CTA-segment tail (round 1: equal chunks only paid off from
@@ -496,8 +500,9 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
     PM_CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->chunk_ev.push_back(e);
   }
-  unsigned long long* slots = c->errw.as<unsigned long long>() + 1;
-  PM_CUDA_TRY(c, cudaMemsetAsync(slots, 0xff, chunks * 8, c->stream));
+  // each chunk's error word sits after the costs and is set to "none" by the
+  // chunk's first kernel (errw_override of evaluate_core)
+  unsigned long long* slots = c->costs_out.as<unsigned long long>() + count;
   // the copies follow everything already queued on the compute stream (the
   // call is ordered like one stream operation: a caller's event recorded
   // before it brackets the whole transfer), and the scratch buffer `words` is
@@ -516,10 +521,10 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
                                  c->costs_out.as<int64_t>() + off, mode, slots + used);
     if (rc != PM_OK) return rc;
   }
-  std::vector<unsigned long long> errs(used);
-  PM_CUDA_TRY(c, cudaMemcpyAsync(costs_out, c->costs_out.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
-  PM_CUDA_TRY(c, cudaMemcpyAsync(errs.data(), slots, used * 8, cudaMemcpyDeviceToHost, c->stream));
+  PM_CUDA_TRY(c, cudaMemcpyAsync(c->hout.p, c->costs_out.p, (count + used) * 8, cudaMemcpyDeviceToHost, c->stream));
   PM_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  std::memcpy(costs_out, c->hout.p, count * 8);
+  const unsigned long long* errs = c->hout.as<unsigned long long>() + count;
   for (int i = 0; i < used; ++i)
     if (errs[i] != ~0ull) {
       if (first_bad) *first_bad = starts[i] + (size_t)errs[i];
@@ -552,7 +557,7 @@ int pm_scan_walks_device(pm_ctx* c, const uint64_t* bitsets_device, size_t count
   PM_CUDA_TRY(c, c->T.ensure(groups * scan_t_stride(c->t.m) * 8));
   PM_CUDA_TRY(c, c->scal.ensure(std::max<size_t>(16, count * 8)));
   PM_CUDA_TRY(c, launch_transpose_population(bitsets_device, count, (int)words_per, c->t.m, c->T.as<uint64_t>(),
-                                             c->scal.as<unsigned long long>(), c->stream));
+                                             c->scal.as<unsigned long long>(), nullptr, c->stream));
   PM_CUDA_TRY(c, cudaMemsetAsync(group_walk_sum_device, 0, (count + 31) / 32 * 8, c->stream));
   PM_CUDA_TRY(c, cudaMemsetAsync(client_max_walk_device, 0, (size_t)c->t.n * 4, c->stream));
   PM_CUDA_TRY(c, launch_walks(c->t, c->T.as<uint64_t>(), count,

@@ -108,6 +108,7 @@ struct pm_ctx {
   // scratch
   DevBuf costs_in, sort_keys, sort_pay, sort_rows, words, costs_out, T, lists, counts, errw, scal;
   DevBuf c16, dT16;  // set_instance scratch: the u16 cost copies of the fused prep pass
+  pmb::HostBuf hout;  // host-buffer calls: costs + error words come back in one pinned copy
   int open_cap = 0;
   GaBuffers ga;
   cudaStream_t copy_stream = nullptr;  // H2D of pipelined host-buffer calls

@@ -61,10 +61,13 @@ __global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __
                                                               size_t count, int wp, int m,
                                                               uint64_t* __restrict__ T,
                                                               size_t Ts,
-                                                              unsigned long long* __restrict__ costs) {
+                                                              unsigned long long* __restrict__ costs,
+                                                              unsigned long long* __restrict__ err_init) {
   const int lane = threadIdx.x & 31;
   const int wi = blockIdx.x * 8 + (threadIdx.x >> 5);
   const size_t groups = (count + 63) / 64;
+  // the call's error word starts at "none" (replaces a memset; the scan runs after)
+  if (err_init && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *err_init = ~0ull;
   // groups stride over gridDim.y (<= 65535) so any population size launches
   for (size_t g = blockIdx.y; g < groups; g += gridDim.y) {
     uint64_t* Tg = T + g * Ts;
@@ -91,10 +94,11 @@ __global__ void __launch_bounds__(256) k_transpose_population(const uint64_t* __
 }
 
 cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int words_per, int m,
-                                        uint64_t* T, unsigned long long* costs, cudaStream_t st) {
+                                        uint64_t* T, unsigned long long* costs, unsigned long long* err_init,
+                                        cudaStream_t st) {
   const size_t groups = (count + 63) / 64;
   dim3 grid((words_per + 7) / 8, (unsigned)std::min<size_t>(groups, 65535));
-  k_transpose_population<<<grid, 256, 0, st>>>(words, count, words_per, m, T, scan_t_stride(m), costs);
+  k_transpose_population<<<grid, 256, 0, st>>>(words, count, words_per, m, T, scan_t_stride(m), costs, err_init);
   return cudaGetLastError();
 }
 

@@ -29,7 +29,10 @@ namespace pmb {
 __global__ void __launch_bounds__(256) k_open_lists(const uint64_t* __restrict__ words, size_t count,
                                                     int wp, int m, uint32_t* __restrict__ lists,
                                                     uint32_t* __restrict__ counts, int cap,
-                                                    unsigned long long* __restrict__ costs) {
+                                                    unsigned long long* __restrict__ costs,
+                                                    unsigned long long* __restrict__ err_init) {
+  // the call's error word starts at "none" (replaces a memset; the gather runs after)
+  if (err_init && blockIdx.x == 0 && threadIdx.x == 0) *err_init = ~0ull;
   const size_t c = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (c >= count) return;
   const int lane = threadIdx.x & 31;
@@ -237,9 +240,9 @@ static cudaError_t launch_gather_t(const DevTables& t, const uint64_t* words, si
 
 cudaError_t launch_open_lists(const uint64_t* words, size_t count, int words_per, int m,
                               uint32_t* open_lists, uint32_t* open_counts, int open_cap,
-                              unsigned long long* costs, cudaStream_t st) {
+                              unsigned long long* costs, unsigned long long* err_init, cudaStream_t st) {
   k_open_lists<<<(unsigned)((count + 7) / 8), 256, 0, st>>>(words, count, words_per, m, open_lists,
-                                                             open_counts, open_cap, costs);
+                                                             open_counts, open_cap, costs, err_init);
   return cudaGetLastError();
 }
 

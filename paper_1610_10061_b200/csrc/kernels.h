@@ -57,8 +57,10 @@ struct DevTables {
 // K2t: population words -> per-group transposed site masks T[g][s] (64 chromosomes / group).
 size_t scan_t_stride(int m);  // u64 entries per group (>= m + 1, even)
 // also zeroes costs[0, count) (the scan accumulates into it)
+// err_init (nullable): an error word the launch sets to ~0 (no failure) first
 cudaError_t launch_transpose_population(const uint64_t* words, size_t count, int words_per, int m,
-                                        uint64_t* T, unsigned long long* costs, cudaStream_t st);
+                                        uint64_t* T, unsigned long long* costs, unsigned long long* err_init,
+                                        cudaStream_t st);
 
 // K2: bit-sliced scan.  costs_acc (count u64) must be zeroed; err_first_bad
 // (u64) must hold ~0 before the launch.
@@ -88,7 +90,7 @@ cudaError_t launch_walks(const DevTables& t, const uint64_t* T, size_t count, un
 // also zeroes costs[0, count) (the gather accumulates into it)
 cudaError_t launch_open_lists(const uint64_t* words, size_t count, int words_per, int m,
                               uint32_t* open_lists, uint32_t* open_counts, int open_cap,
-                              unsigned long long* costs, cudaStream_t st);
+                              unsigned long long* costs, unsigned long long* err_init, cudaStream_t st);
 // K2b: gather-min (needs launch_open_lists first).  mode 0 = fitness semantics (scan-width contract), 1 = min_cost_sum.
 cudaError_t launch_gather(const DevTables& t, const uint64_t* words, size_t count, int words_per,
                           uint32_t* open_lists, uint32_t* open_counts, int open_cap,
