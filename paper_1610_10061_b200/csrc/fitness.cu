@@ -211,7 +211,7 @@ struct MaskOps {
 // kW > 0: the many-warp variant -- kW warps per SM in CTAs of kCtaW warps
 // (registers capped at 64K / (32 kW)), a kWQ-record queue, two row chunks.
 template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kDepth, int kW = 0, int kWQ = 128,
-          int kCtaW = kW>
+          int kCtaW = kW, bool kPairCols = false>
 __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCtaW : 1) : 1)
     k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
            const uint64_t* __restrict__ T, size_t Ts, size_t count, int groups,
@@ -252,6 +252,8 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
   constexpr bool kSplitQ = kPacked && (PMB_X_SPLITQ || (PMB_X_SHORT && kShortCta));
   constexpr bool kFlo = PMB_X_BFIND || (PMB_X_SHORT && kShortCta);
   constexpr bool kRawCost = kSplitQ && !kDepth && sizeof(DistT) == 2 && sizeof(AccT) == 4;
+  // column pairs (plan_scan: long walks only): one ballot per two columns
+  constexpr bool kPair = kPairCols && kPacked && !kSplitQ && kW > 0 && !kShortCta && !kDepth;
 
   const long long U = (long long)groups * n;
   long long u = U * blockIdx.x / gridDim.x;
@@ -389,35 +391,60 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
         __syncwarp();  // the queue is rewritten next
       };
       uint32_t qn = 0;  // warp-uniform queue length
+      if constexpr (kPair) {
+        // column pairs: one ballot per pair, and a lane with a hit in either
+        // column appends both columns' records with one 16-byte store (an empty
+        // mask drains as a no-op)
 #pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        if constexpr (kQ < kChunk * 32) {
-          // every kQCheck columns (warp-uniform): the next kQCheck columns could overflow
-          if (j % kQCheck == 0 && qn > (uint32_t)(kQ - 32 * kQCheck)) {
+        for (int j = 0; j < kChunk; j += 2) {
+          if (qn > (uint32_t)(kQ - 64)) {
             drain(qn);
             qn = 0;
           }
-        }
-        const MaskT h = alive & t[j];
-        alive &= ~t[j];
-        const unsigned hb = __ballot_sync(kFull, h != 0);
-        if (h) {
-          // kDepth: the 1-based stopping column k* instead of the cost
-          // (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
-          AccT dval;
-          if constexpr (kDepth) dval = (AccT)(k + j + 1);
-          else if constexpr (kRawCost) dval = (AccT)cur.cost_raw(j);
-          else dval = (AccT)cur.cost(j);
-          const uint32_t q = qn + __popc(hb & lt);
-          PMB_CHECK(q < (uint32_t)kQ);
-          if constexpr (kPacked && !kSplitQ) {
-            wq[q] = (uint64_t)h | ((uint64_t)dval << 32);
-          } else {
-            wqh[q] = h;
-            wqd[q] = dval;
+          const MaskT h0 = alive & t[j];
+          alive &= ~t[j];
+          const MaskT h1 = alive & t[j + 1];
+          alive &= ~t[j + 1];
+          const unsigned hb = __ballot_sync(kFull, (h0 | h1) != 0);
+          if (h0 | h1) {
+            const uint32_t q = qn + 2 * __popc(hb & lt);
+            PMB_CHECK(q + 1 < (uint32_t)kQ);
+            *reinterpret_cast<uint4*>(wq + q) =
+                make_uint4((uint32_t)h0, (uint32_t)cur.cost(j), (uint32_t)h1, (uint32_t)cur.cost(j + 1));
           }
+          qn += 2 * __popc(hb);
         }
-        qn += __popc(hb);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          if constexpr (kQ < kChunk * 32) {
+            // every kQCheck columns (warp-uniform): the next kQCheck columns could overflow
+            if (j % kQCheck == 0 && qn > (uint32_t)(kQ - 32 * kQCheck)) {
+              drain(qn);
+              qn = 0;
+            }
+          }
+          const MaskT h = alive & t[j];
+          alive &= ~t[j];
+          const unsigned hb = __ballot_sync(kFull, h != 0);
+          if (h) {
+            // kDepth: the 1-based stopping column k* instead of the cost
+            // (B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
+            AccT dval;
+            if constexpr (kDepth) dval = (AccT)(k + j + 1);
+            else if constexpr (kRawCost) dval = (AccT)cur.cost_raw(j);
+            else dval = (AccT)cur.cost(j);
+            const uint32_t q = qn + __popc(hb & lt);
+            PMB_CHECK(q < (uint32_t)kQ);
+            if constexpr (kPacked && !kSplitQ) {
+              wq[q] = (uint64_t)h | ((uint64_t)dval << 32);
+            } else {
+              wqh[q] = h;
+              wqd[q] = dval;
+            }
+          }
+          qn += __popc(hb);
+        }
       }
       drain(qn);
       if (i >= 0) {
@@ -482,9 +509,12 @@ static const void* scan_fn_acc(int G, bool tsmem) {
                  : scan_fn_depth<OrdT, DistT, AccT, false>(G, tsmem);
 }
 
-static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool ts, int wide = 0) {
+static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool ts, int wide = 0,
+                                   bool pair = false) {
   if (wide && t.site_bytes == 2 && t.dist_bytes == 2 && acc32 && G == 32 && ts && !g_depth) {
     // wide = warps per CTA of the variant (kWideWarps: one CTA per SM)
+    if (pair && wide == kWideWarps)
+      return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue, kWideWarps, true>);
     if (wide == 2) return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue, 2>);
     if (wide == 4) return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue, 4>);
     return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue>);
@@ -573,6 +603,13 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
             sp.warps = kWideWarps;
             sp.ctas = sms;
             sp.smem = sm2;
+            // long walks (m >= 75 p: few open sites, so few hits per column):
+            // column pairs -- one ballot and one 16-byte queue store per two
+            // columns.  syn20k 1.41 -> 1.40 ms, sweep p=50 1.42 -> 1.31 ms,
+            // p=100 0.78 -> 0.76 ms; at p >= 200 the extra empty records of
+            // the denser hits cost more (0.46 -> 0.48 ms) (profiles/r02_k2_ab.md)
+            const char* ep = getenv("PMB_SCAN_PAIR");
+            sp.pair = ep ? ep[0] == '1' : (long long)t.m >= 75LL * std::max(t.p, 1);
           }
         }
         // split shapes (short segments): the same variant as 12 x 2-warp (or
@@ -605,7 +642,7 @@ cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* 
                         unsigned long long* costs_acc, unsigned long long* err_first_bad,
                         int depth_mode, cudaStream_t st) {
   g_depth = depth_mode != 0;
-  const void* fn = scan_kernel_ptr(t, sp.acc32, sp.G, sp.tsmem, sp.wide);
+  const void* fn = scan_kernel_ptr(t, sp.acc32, sp.G, sp.tsmem, sp.wide, sp.pair);
   // raise the kernel's dynamic shared-memory cap only when it grows (the call
   // costs host time on every launch otherwise; the GA launches K2 ~10x per generation)
   static thread_local std::vector<std::pair<const void*, size_t>> raised;

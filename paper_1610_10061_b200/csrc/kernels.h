@@ -72,6 +72,7 @@ struct ScanPlan {
   int G = 64;         // chromosomes per group (64 or 32)
   size_t smem = 0;
   int wide = 0;       // 1: the many-warp variant (kWideWarps per CTA, kWideQueue records, 2 row chunks)
+  bool pair = false;  // the 24-warp variant appends column pairs (long walks)
 };
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode);
 // depth_mode != 0 accumulates the 1-based stopping columns k* instead of costs.
