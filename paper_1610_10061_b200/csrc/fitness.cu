@@ -125,7 +125,8 @@ constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
 #ifndef PMB_X_SHORT
 #define PMB_X_SHORT 1
 #endif
-constexpr int kWideWarps = 24, kWideQueue = 256;  // the many-warp K2 variant (plan_scan)
+constexpr int kWideWarps = 24, kWideQueue = 256;
+constexpr double kCoopGain = 1.3;  // plan_scan's cooperative-tail threshold factor  // the many-warp K2 variant (plan_scan)
 #ifndef PMB_QCHECK
 #define PMB_QCHECK 2
 #endif
@@ -215,7 +216,7 @@ template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kD
 __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCtaW : 1) : 1)
     k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
            const uint64_t* __restrict__ T, size_t Ts, size_t count, int groups,
-           unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err) {
+           unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err, int coop) {
   using Ops = MaskOps<MaskT>;
   constexpr int kG = Ops::kG;
   // row chunks in registers: 3 (two in flight while one is consumed) when the
@@ -313,9 +314,112 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
     int wb_next = 0, wb_end = 0;
     bool exhausted = false;
 
+    // drain: lane r applies queue records r, r+32, ... -- the loop runs the
+    // largest record's bit count, not the busiest lane's hit count
+    auto drain = [&](uint32_t qn) {
+      __syncwarp();  // queue writes visible to the draining lanes
+      for (uint32_t base = 0; base < qn; base += 32) {
+        MaskT h = 0;
+        AccT dv = 0;
+        if (base + lane < qn) {
+          if constexpr (kPacked && !kSplitQ) {
+            const uint64_t x = wq[base + lane];
+            h = (MaskT)x;
+            dv = (AccT)(x >> 32);
+          } else {
+            h = wqh[base + lane];
+            dv = wqd[base + lane];
+          }
+          if constexpr (kRawCost) dv &= 0xffffu;
+        }
+        while (h) {
+          const int c = Ops::template pop_high<kFlo>(h);
+#if PMB_X_RED
+          // a shared-memory reduction: lane-private column (no contention),
+          // and the lane does not wait for a load-add-store round trip
+          if constexpr (sizeof(AccT) == 4) atomicAdd(reinterpret_cast<unsigned*>(myacc + c * 32), (unsigned)dv);
+          else atomicAdd(reinterpret_cast<unsigned long long*>(myacc + c * 32), (unsigned long long)dv);
+#else
+          myacc[c * 32] += dv;
+#endif
+        }
+      }
+      __syncwarp();  // the queue is rewritten next
+    };
+    // the 16 masks of chunk `cur` (idle lanes hold sentinel sites: zero masks)
+    auto lookup = [&](const Chunk<OrdT, DistT>& cur, MaskT (&t)[kChunk]) {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        PMB_CHECK(cur.site(j) < Ts);
+        if constexpr (kTSmem) t[j] = Tsm[cur.site(j)];
+        else t[j] = (MaskT)(__ldg(Tg + cur.site(j)) >> half);
+      }
+    };
+    // the column phase of one chunk: walk `al` over the masks, appending hit
+    // columns to the warp queue, then drain it; kb = the chunk's first column
+    auto columns = [&](const Chunk<OrdT, DistT>& cur, const MaskT (&t)[kChunk], MaskT& al, int kb) {
+      uint32_t qn = 0;  // warp-uniform queue length
+      if constexpr (kPair) {
+        // column pairs: one ballot per pair, and a lane with a hit in either
+        // column appends both columns' records with one 16-byte store (an empty
+        // mask drains as a no-op)
+#pragma unroll
+        for (int j = 0; j < kChunk; j += 2) {
+          if (qn > (uint32_t)(kQ - 64)) {
+            drain(qn);
+            qn = 0;
+          }
+          const MaskT h0 = al & t[j];
+          al &= ~t[j];
+          const MaskT h1 = al & t[j + 1];
+          al &= ~t[j + 1];
+          const unsigned hb = __ballot_sync(kFull, (h0 | h1) != 0);
+          if (h0 | h1) {
+            const uint32_t q = qn + 2 * __popc(hb & lt);
+            PMB_CHECK(q + 1 < (uint32_t)kQ);
+            *reinterpret_cast<uint4*>(wq + q) =
+                make_uint4((uint32_t)h0, (uint32_t)cur.cost(j), (uint32_t)h1, (uint32_t)cur.cost(j + 1));
+          }
+          qn += 2 * __popc(hb);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          if constexpr (kQ < kChunk * 32) {
+            // every kQCheck columns (warp-uniform): the next kQCheck columns could overflow
+            if (j % kQCheck == 0 && qn > (uint32_t)(kQ - 32 * kQCheck)) {
+              drain(qn);
+              qn = 0;
+            }
+          }
+          const MaskT h = al & t[j];
+          al &= ~t[j];
+          const unsigned hb = __ballot_sync(kFull, h != 0);
+          if (h) {
+            // kDepth: the 1-based stopping column k* instead of the cost
+            // (SURVEY.md 8(d): B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
+            AccT dval;
+            if constexpr (kDepth) dval = (AccT)(kb + j + 1);
+            else if constexpr (kRawCost) dval = (AccT)cur.cost_raw(j);
+            else dval = (AccT)cur.cost(j);
+            const uint32_t q = qn + __popc(hb & lt);
+            PMB_CHECK(q < (uint32_t)kQ);
+            if constexpr (kPacked && !kSplitQ) {
+              wq[q] = (uint64_t)h | ((uint64_t)dval << 32);
+            } else {
+              wqh[q] = h;
+              wqd[q] = dval;
+            }
+          }
+          qn += __popc(hb);
+        }
+      }
+      drain(qn);
+    };
     // One 16-column step on chunk `cur`; `nxt` already holds the following
     // chunk and `cur` is refilled with the one after it.  Returns false once
-    // the warp has no client left.
+    // the warp has no client left (or at most `coop` once the segment's
+    // clients are all claimed: the cooperative tail below takes them).
     auto step = [&](Chunk<OrdT, DistT>& cur, Chunk<OrdT, DistT>& nxt,
                     Chunk<OrdT, DistT>& nxt2) -> bool {
       unsigned need = __ballot_sync(kFull, i < 0);
@@ -347,106 +451,16 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
         wb_next += min(__popc(need), avail);
         need = __ballot_sync(kFull, i < 0);
       }
-      if (__ballot_sync(kFull, i >= 0) == 0) return false;
+      {
+        const unsigned busy = __ballot_sync(kFull, i >= 0);
+        if (busy == 0 || (exhausted && __popc(busy) <= coop)) return false;
+      }
       // Every lane runs the column phase (idle lanes hold sentinel sites and
       // alive == 0), so the warp can append its hit columns to one queue with
       // ballots instead of per-lane slots.
       MaskT t[kChunk];
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        PMB_CHECK(cur.site(j) < Ts);
-        if constexpr (kTSmem) t[j] = Tsm[cur.site(j)];
-        else t[j] = (MaskT)(__ldg(Tg + cur.site(j)) >> half);
-      }
-      // drain: lane r applies queue records r, r+32, ... -- the loop runs the
-      // largest record's bit count, not the busiest lane's hit count
-      auto drain = [&](uint32_t qn) {
-        __syncwarp();  // queue writes visible to the draining lanes
-        for (uint32_t base = 0; base < qn; base += 32) {
-          MaskT h = 0;
-          AccT dv = 0;
-          if (base + lane < qn) {
-            if constexpr (kPacked && !kSplitQ) {
-              const uint64_t x = wq[base + lane];
-              h = (MaskT)x;
-              dv = (AccT)(x >> 32);
-            } else {
-              h = wqh[base + lane];
-              dv = wqd[base + lane];
-            }
-            if constexpr (kRawCost) dv &= 0xffffu;
-          }
-          while (h) {
-            const int c = Ops::template pop_high<kFlo>(h);
-#if PMB_X_RED
-            // a shared-memory reduction: lane-private column (no contention),
-            // and the lane does not wait for a load-add-store round trip
-            if constexpr (sizeof(AccT) == 4) atomicAdd(reinterpret_cast<unsigned*>(myacc + c * 32), (unsigned)dv);
-            else atomicAdd(reinterpret_cast<unsigned long long*>(myacc + c * 32), (unsigned long long)dv);
-#else
-            myacc[c * 32] += dv;
-#endif
-          }
-        }
-        __syncwarp();  // the queue is rewritten next
-      };
-      uint32_t qn = 0;  // warp-uniform queue length
-      if constexpr (kPair) {
-        // column pairs: one ballot per pair, and a lane with a hit in either
-        // column appends both columns' records with one 16-byte store (an empty
-        // mask drains as a no-op)
-#pragma unroll
-        for (int j = 0; j < kChunk; j += 2) {
-          if (qn > (uint32_t)(kQ - 64)) {
-            drain(qn);
-            qn = 0;
-          }
-          const MaskT h0 = alive & t[j];
-          alive &= ~t[j];
-          const MaskT h1 = alive & t[j + 1];
-          alive &= ~t[j + 1];
-          const unsigned hb = __ballot_sync(kFull, (h0 | h1) != 0);
-          if (h0 | h1) {
-            const uint32_t q = qn + 2 * __popc(hb & lt);
-            PMB_CHECK(q + 1 < (uint32_t)kQ);
-            *reinterpret_cast<uint4*>(wq + q) =
-                make_uint4((uint32_t)h0, (uint32_t)cur.cost(j), (uint32_t)h1, (uint32_t)cur.cost(j + 1));
-          }
-          qn += 2 * __popc(hb);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          if constexpr (kQ < kChunk * 32) {
-            // every kQCheck columns (warp-uniform): the next kQCheck columns could overflow
-            if (j % kQCheck == 0 && qn > (uint32_t)(kQ - 32 * kQCheck)) {
-              drain(qn);
-              qn = 0;
-            }
-          }
-          const MaskT h = alive & t[j];
-          alive &= ~t[j];
-          const unsigned hb = __ballot_sync(kFull, h != 0);
-          if (h) {
-            // kDepth: the 1-based stopping column k* instead of the cost
-            // (SURVEY.md 8(d): B_eval = 12 * sum_i k*_i + 8 * ceil(m/64))
-            AccT dval;
-            if constexpr (kDepth) dval = (AccT)(k + j + 1);
-            else if constexpr (kRawCost) dval = (AccT)cur.cost_raw(j);
-            else dval = (AccT)cur.cost(j);
-            const uint32_t q = qn + __popc(hb & lt);
-            PMB_CHECK(q < (uint32_t)kQ);
-            if constexpr (kPacked && !kSplitQ) {
-              wq[q] = (uint64_t)h | ((uint64_t)dval << 32);
-            } else {
-              wqh[q] = h;
-              wqd[q] = dval;
-            }
-          }
-          qn += __popc(hb);
-        }
-      }
-      drain(qn);
+      lookup(cur, t);
+      columns(cur, t, alive, k);
       if (i >= 0) {
         k += kChunk;
         if (alive == 0 || k >= Wp) {
@@ -470,6 +484,55 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
       }
     } else {
       while (step(ca, cb, cb) && step(cb, ca, ca)) {
+      }
+    }
+    {
+      // Cooperative tail.  Once the segment's clients are all claimed, a warp
+      // with few clients left would step 16 columns at a time with most lanes
+      // idle until its longest walk ends (the walk of the last of 32
+      // chromosomes, ~(m/p) H_32 columns: the launch tail).  Instead the whole
+      // warp walks each remaining client in turn, lane r taking columns
+      // [k + 16 r, k + 16 r + 16): a chromosome's first open site is in the
+      // lowest lane whose columns hold one, so lane r walks with the
+      // chromosomes no lower lane hits (an exclusive OR-scan of the lanes'
+      // hit unions) and the records are exactly those of the sequential walk.
+      unsigned rest = __ballot_sync(kFull, i >= 0);
+      while (rest) {
+        const int L = __ffs(rest) - 1;
+        rest &= rest - 1;
+        const int ci = __shfl_sync(kFull, i, L);
+        int ck = __shfl_sync(kFull, k, L);
+        MaskT A = __shfl_sync(kFull, alive, L);
+        const OrdT* corow = ord + (size_t)ci * Wp;
+        const DistT* cdrow = dist + (size_t)ci * Wp;
+        for (;;) {
+          const int kk = ck + lane * kChunk;
+          if (kk < Wp) ca.load(corow, cdrow, kk);
+          else ca.set_sentinel(sentinel);
+          MaskT t[kChunk];
+          lookup(ca, t);
+          MaskT U = 0;
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j) U |= t[j];
+          U &= A;
+          MaskT P = U;  // inclusive OR over lanes <= lane
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const MaskT v = __shfl_up_sync(kFull, P, o);
+            if (lane >= o) P |= v;
+          }
+          MaskT below = __shfl_up_sync(kFull, P, 1);
+          if (lane == 0) below = 0;
+          MaskT al = A & ~below;
+          columns(ca, t, al, kk);
+          A &= ~__shfl_sync(kFull, P, 31);
+          ck += 32 * kChunk;
+          if (A == 0) break;
+          if (ck >= Wp) {  // runoff: no open site within the row
+            if (lane == 0) atomicMin(err, (unsigned long long)g * kG + Ops::low_index(A));
+            break;
+          }
+        }
       }
     }
     __syncthreads();
@@ -630,6 +693,14 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
             }
           }
         }
+        // cooperative tail (k_scan): a warp hands its last clients to the
+        // whole warp once at most `coop` are left.  A cooperative pass costs
+        // about one 16-column step and advances one client 512 columns, so it
+        // pays while fewer clients remain than steps left in the last walk,
+        // ~(m/p)/16 (the last chromosome's wait for an open site)
+        const char* ec = getenv("PMB_SCAN_COOP");
+        sp.coop = ec ? std::atoi(ec)
+                     : (int)std::min<double>(32.0, kCoopGain * t.m / (16.0 * std::max(t.p, 1)));
         return sp;
       }
     }
@@ -661,9 +732,9 @@ cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* 
   size_t Ts = scan_t_stride(t.m);
   const void* ord = t.ord;
   const void* dist = t.dist;
-  int n = t.n, Wp = t.Wp;
+  int n = t.n, Wp = t.Wp, coop = sp.coop;
   void* args[] = {(void*)&ord, (void*)&dist, (void*)&n, (void*)&Wp, (void*)&T, (void*)&Ts,
-                  (void*)&count, (void*)&groups, (void*)&costs_acc, (void*)&err_first_bad};
+                  (void*)&count, (void*)&groups, (void*)&costs_acc, (void*)&err_first_bad, (void*)&coop};
   e = cudaLaunchKernel(fn, dim3(ctas), dim3(sp.warps * 32), args, sp.smem, st);
   return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -73,6 +73,7 @@ struct ScanPlan {
   size_t smem = 0;
   int wide = 0;       // 1: the many-warp variant (kWideWarps per CTA, kWideQueue records, 2 row chunks)
   bool pair = false;  // the 24-warp variant appends column pairs (long walks)
+  int coop = 0;       // clients per warp at or below which the tail walks them cooperatively
 };
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode);
 // depth_mode != 0 accumulates the 1-based stopping columns k* instead of costs.

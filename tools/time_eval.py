@@ -18,7 +18,7 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 shapes = (sys.argv[4] if len(sys.argv) > 4 else "auto").split()
 rounds = int(sys.argv[5]) if len(sys.argv) > 5 else 2
 n = m = cfg["npts"]
-p, count = cfg["p"], cfg["count"]
+p, count = cfg["p"], int(os.environ.get("TE_COUNT") or cfg["count"])  # TE_COUNT: a shard-sized batch
 wp = (m + 63) // 64
 ctx = pm.Context(0)
 s = torch.cuda.Stream()
@@ -64,4 +64,4 @@ for r in range(rounds):
             ms, nl = ctx.profile_read()
             ctx.set_profiling(False)
         print(f"{cfg['workload'][:6]} kind={kind} shape={sh} kernel_ms={ms/nl:.3f} "
-              f"evals/s={count/(ms/nl/1e3):.0f} clk={clock()}", flush=True)
+              f"evals/s={count/(ms/nl/1e3):.0f} sum={int(out.sum())} clk={clock()}", flush=True)
