@@ -126,7 +126,8 @@ constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
 #define PMB_X_SHORT 1
 #endif
 constexpr int kWideWarps = 24, kWideQueue = 256;
-constexpr double kCoopGain = 1.3;  // plan_scan's cooperative-tail threshold factor  // the many-warp K2 variant (plan_scan)
+constexpr double kCoopGain = 1.3;  // plan_scan's cooperative-tail threshold factor
+constexpr int kTailClaim = 32;      // clients left per warp below which claims shrink (tools/env_ab.sh)  // the many-warp K2 variant (plan_scan)
 #ifndef PMB_QCHECK
 #define PMB_QCHECK 2
 #endif
@@ -216,7 +217,8 @@ template <class OrdT, class DistT, class AccT, class MaskT, bool kTSmem, bool kD
 __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCtaW : 1) : 1)
     k_scan(const OrdT* __restrict__ ord, const DistT* __restrict__ dist, int n, int Wp,
            const uint64_t* __restrict__ T, size_t Ts, size_t count, int groups,
-           unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err, int coop) {
+           unsigned long long* __restrict__ costs, unsigned long long* __restrict__ err, int coop,
+           int tail_claim) {
   using Ops = MaskOps<MaskT>;
   constexpr int kG = Ops::kG;
   // row chunks in registers: 3 (two in flight while one is consumed) when the
@@ -425,15 +427,22 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
       unsigned need = __ballot_sync(kFull, i < 0);
       while (need && !exhausted) {  // warp-uniform client claiming
         if (wb_next >= wb_end) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(next_client, 32);
+          // batches of 32 clients, but only as many as lanes need once fewer
+          // than tail_claim are left: a warp holding a private batch while the
+          // others run dry stretches the segment's tail
+          int base = 0, take = 32;
+          if (lane == 0) {
+            if (c1 - *reinterpret_cast<volatile int*>(next_client) < tail_claim) take = __popc(need);
+            base = atomicAdd(next_client, take);
+          }
           base = __shfl_sync(kFull, base, 0);
+          take = __shfl_sync(kFull, take, 0);
           if (base >= c1) {
             exhausted = true;
             break;
           }
           wb_next = base;
-          wb_end = min(base + 32, c1);
+          wb_end = min(base + take, c1);
         }
         const int rank = __popc(need & lt);
         const int avail = wb_end - wb_next;
@@ -701,6 +710,8 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
         const char* ec = getenv("PMB_SCAN_COOP");
         sp.coop = ec ? std::atoi(ec)
                      : (int)std::min<double>(32.0, kCoopGain * t.m / (16.0 * std::max(t.p, 1)));
+        const char* et = getenv("PMB_SCAN_TAILCLAIM");  // clients left per warp (x warps)
+        sp.tail_claim = (et ? std::atoi(et) : kTailClaim) * sp.warps;
         return sp;
       }
     }
@@ -732,9 +743,10 @@ cudaError_t launch_scan(const DevTables& t, const ScanPlan& sp, const uint64_t* 
   size_t Ts = scan_t_stride(t.m);
   const void* ord = t.ord;
   const void* dist = t.dist;
-  int n = t.n, Wp = t.Wp, coop = sp.coop;
+  int n = t.n, Wp = t.Wp, coop = sp.coop, tail_claim = sp.tail_claim;
   void* args[] = {(void*)&ord, (void*)&dist, (void*)&n, (void*)&Wp, (void*)&T, (void*)&Ts,
-                  (void*)&count, (void*)&groups, (void*)&costs_acc, (void*)&err_first_bad, (void*)&coop};
+                  (void*)&count, (void*)&groups, (void*)&costs_acc, (void*)&err_first_bad, (void*)&coop,
+                  (void*)&tail_claim};
   e = cudaLaunchKernel(fn, dim3(ctas), dim3(sp.warps * 32), args, sp.smem, st);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
