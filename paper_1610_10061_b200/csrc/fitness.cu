@@ -125,9 +125,9 @@ constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
 #ifndef PMB_X_SHORT
 #define PMB_X_SHORT 1
 #endif
-constexpr int kWideWarps = 24, kWideQueue = 256;
+constexpr int kWideWarps = 24, kWideQueue = 256;  // the many-warp K2 variant (plan_scan)
 constexpr double kCoopGain = 1.3;  // plan_scan's cooperative-tail threshold factor
-constexpr int kTailClaim = 32;      // clients left per warp below which claims shrink (tools/env_ab.sh)  // the many-warp K2 variant (plan_scan)
+constexpr int kTailClaim = 32;     // clients left per warp below which claims shrink (tools/env_ab.sh)
 #ifndef PMB_QCHECK
 #define PMB_QCHECK 2
 #endif
