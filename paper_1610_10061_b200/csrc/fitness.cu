@@ -126,7 +126,7 @@ constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
 #define PMB_X_SHORT 1
 #endif
 constexpr int kWideWarps = 24, kWideQueue = 256;  // the many-warp K2 variant (plan_scan)
-constexpr double kCoopGain = 1.3;  // plan_scan's cooperative-tail threshold factor
+constexpr int kCoop = 16;          // clients per warp at which the cooperative tail starts
 constexpr int kTailClaim = 32;     // clients left per warp below which claims shrink (tools/env_ab.sh)
 #ifndef PMB_QCHECK
 #define PMB_QCHECK 2
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
       }
       {
         const unsigned busy = __ballot_sync(kFull, i >= 0);
-        if (busy == 0 || (exhausted && __popc(busy) <= coop)) return false;
+        if (busy == 0 || (exhausted && __popc(busy) <= (coop & 0xff))) return false;
       }
       // Every lane runs the column phase (idle lanes hold sentinel sites and
       // alive == 0), so the warp can append its hit columns to one queue with
@@ -499,24 +499,32 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
       // Cooperative tail.  Once the segment's clients are all claimed, a warp
       // with few clients left would step 16 columns at a time with most lanes
       // idle until its longest walk ends (the walk of the last of 32
-      // chromosomes, ~(m/p) H_32 columns: the launch tail).  Instead the whole
-      // warp walks each remaining client in turn, lane r taking columns
-      // [k + 16 r, k + 16 r + 16): a chromosome's first open site is in the
-      // lowest lane whose columns hold one, so lane r walks with the
-      // chromosomes no lower lane hits (an exclusive OR-scan of the lanes'
-      // hit unions) and the records are exactly those of the sequential walk.
-      unsigned rest = __ballot_sync(kFull, i >= 0);
-      while (rest) {
-        const int L = __ffs(rest) - 1;
-        rest &= rest - 1;
-        const int ci = __shfl_sync(kFull, i, L);
-        int ck = __shfl_sync(kFull, k, L);
-        MaskT A = __shfl_sync(kFull, alive, L);
-        const OrdT* corow = ord + (size_t)ci * Wp;
-        const DistT* cdrow = dist + (size_t)ci * Wp;
+      // chromosomes, ~(m/p) H_32 columns: the launch tail).  Instead (at most
+      // coop & 0xff clients left) the clients walk side by side, each on a
+      // segment of S lanes -- the largest power of two with S x clients <= 32,
+      // at most 1 << (coop >> 8) -- lane r of a segment taking columns
+      // [k + 16 r, k + 16 r + 16), re-packed every pass as clients finish.  A
+      // chromosome's first open site is in the lowest lane whose columns hold
+      // one, so lane r walks with the chromosomes no lower lane of its segment
+      // hits (an exclusive OR-scan of the lanes' hit unions) and the records
+      // are exactly those of the sequential walk.
+      {
+        const int lg_max = (coop >> 8) & 31;
         for (;;) {
-          const int kk = ck + lane * kChunk;
-          if (kk < Wp) ca.load(corow, cdrow, kk);
+          const unsigned act = __ballot_sync(kFull, i >= 0);
+          if (act == 0) break;
+          const int na = __popc(act);
+          const int lgS = min(lg_max, 5 - (32 - __clz(na - 1)));
+          const int S = 1 << lgS;
+          const int seg = lane >> lgS, sl = lane & (S - 1);
+          const bool on = seg < na;
+          const int L = on ? (int)__fns(act, 0, seg + 1) : 0;
+          const int ci = __shfl_sync(kFull, i, L);
+          const int ck = __shfl_sync(kFull, k, L);
+          MaskT A = __shfl_sync(kFull, alive, L);
+          if (!on) A = 0;
+          const int kk = ck + sl * kChunk;
+          if (on && kk < Wp) ca.load(ord + (size_t)ci * Wp, dist + (size_t)ci * Wp, kk);
           else ca.set_sentinel(sentinel);
           MaskT t[kChunk];
           lookup(ca, t);
@@ -524,22 +532,26 @@ __global__ void __launch_bounds__(kW ? kCtaW * 32 : 512, kW ? kW / (kCtaW ? kCta
 #pragma unroll
           for (int j = 0; j < kChunk; ++j) U |= t[j];
           U &= A;
-          MaskT P = U;  // inclusive OR over lanes <= lane
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const MaskT v = __shfl_up_sync(kFull, P, o);
-            if (lane >= o) P |= v;
+          MaskT P = U;  // inclusive OR over the segment's lanes <= sl
+          for (int o = 1; o < S; o <<= 1) {
+            const MaskT v = __shfl_up_sync(kFull, P, o, S);
+            if (sl >= o) P |= v;
           }
-          MaskT below = __shfl_up_sync(kFull, P, 1);
-          if (lane == 0) below = 0;
+          MaskT below = __shfl_up_sync(kFull, P, 1, S);
+          if (sl == 0) below = 0;
           MaskT al = A & ~below;
           columns(ca, t, al, kk);
-          A &= ~__shfl_sync(kFull, P, 31);
-          ck += 32 * kChunk;
-          if (A == 0) break;
-          if (ck >= Wp) {  // runoff: no open site within the row
-            if (lane == 0) atomicMin(err, (unsigned long long)g * kG + Ops::low_index(A));
-            break;
+          const MaskT left = A & ~__shfl_sync(kFull, P, S - 1, S);  // uniform in the segment
+          // back to the owning lanes: the client of rank r walked on segment r
+          const MaskT got = __shfl_sync(kFull, left, (__popc(act & lt) << lgS) & 31);
+          if (i >= 0) {
+            k += S * kChunk;
+            alive = got;
+            if (alive == 0 || k >= Wp) {
+              if (alive) atomicMin(err, (unsigned long long)g * kG + Ops::low_index(alive));
+              i = -1;
+              alive = 0;
+            }
           }
         }
       }
@@ -702,14 +714,13 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
             }
           }
         }
-        // cooperative tail (k_scan): a warp hands its last clients to the
-        // whole warp once at most `coop` are left.  A cooperative pass costs
-        // about one 16-column step and advances one client 512 columns, so it
-        // pays while fewer clients remain than steps left in the last walk,
-        // ~(m/p)/16 (the last chromosome's wait for an open site)
+        // cooperative tail (k_scan): a warp's last <= kCoop clients walk on
+        // lane segments (profiles/r02_k2_ab.md; PMB_SCAN_COOP=<clients> and
+        // PMB_SCAN_COOPSEG=<log2 most lanes per client> for A/B runs)
         const char* ec = getenv("PMB_SCAN_COOP");
-        sp.coop = ec ? std::atoi(ec)
-                     : (int)std::min<double>(32.0, kCoopGain * t.m / (16.0 * std::max(t.p, 1)));
+        const char* es = getenv("PMB_SCAN_COOPSEG");
+        sp.coop = std::min(32, std::max(0, ec ? std::atoi(ec) : kCoop)) |
+                  (std::min(5, std::max(0, es ? std::atoi(es) : 5)) << 8);
         const char* et = getenv("PMB_SCAN_TAILCLAIM");  // clients left per warp (x warps)
         sp.tail_claim = (et ? std::atoi(et) : kTailClaim) * sp.warps;
         return sp;

@@ -73,7 +73,7 @@ struct ScanPlan {
   size_t smem = 0;
   int wide = 0;       // 1: the many-warp variant (kWideWarps per CTA, kWideQueue records, 2 row chunks)
   bool pair = false;  // the 24-warp variant appends column pairs (long walks)
-  int coop = 0;       // clients per warp at or below which the tail walks them cooperatively
+  int coop = 0;       // cooperative tail: clients per warp at which it starts | log2(max lanes per client) << 8
   int tail_claim = 0; // clients left in a segment below which a warp claims only what its lanes need
 };
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode);
