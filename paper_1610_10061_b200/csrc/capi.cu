@@ -347,13 +347,13 @@ static bool scan_fits(pm_ctx* c, size_t count) {
 }
 
 // Measured crossover (profiles/r02_p_sweep.md): the scan touches
-// ~(m+1)/(p+1) columns per client (time ~ a m / p), the gather p sites (time
-// ~ b p), so they meet at p* = sqrt(a m / b); the n=m=10000 sweep with the
-// 8-deep gather puts it at p* = 101 (scan 0.783 ms vs gather 0.761 ms at
-// p = 100), i.e. p* ~ 1.01 sqrt(m).
+// ~(m+1)/(p+1) columns per client (time ~ a m / p + c), the gather p sites
+// (time ~ b p), so they meet near p* ~ sqrt(a m / b); the n=m=10000 sweep
+// (scan 1.177 / 0.701 ms, gather 0.479 / 0.805 ms at p = 50 / 100) puts it at
+// p* = 93, i.e. p* ~ 0.93 sqrt(m).
 static int auto_kind(pm_ctx* c, size_t count) {
   if (!scan_fits(c, count)) return PM_EVAL_GATHER;
-  const double pstar = 1.01 * std::sqrt((double)c->t.m);
+  const double pstar = 0.93 * std::sqrt((double)c->t.m);
   return (double)c->t.p >= pstar ? PM_EVAL_SCAN : PM_EVAL_GATHER;
 }
 
