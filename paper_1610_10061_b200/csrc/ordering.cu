@@ -489,17 +489,16 @@ __device__ __forceinline__ void for_each_cost(const CostT* __restrict__ crow, in
   }
 }
 
-template <class OrdT, class DistT, class CostT, bool kWin>
+template <class OrdT, class DistT, class CostT>
 __global__ void __launch_bounds__(kCsThreads, 2)
     k_build_rows_cs(const CostT* __restrict__ costs, int cstride, int n, int m, int W, int Wp, int sitebits,
                     int costbits, OrdT* __restrict__ ord, DistT* __restrict__ dist, int* __restrict__ rows) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t wsum[kCsThreads / 32];
-  __shared__ int flag, nfix;
+  __shared__ int flag;
   const int nb = 1 << costbits, nw = nb >> 1;  // buckets; u32 words of two u16 counters
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
   uint32_t* out = cnt + nw;  // the sorted row, packed (cost << sitebits | site)
-  uint16_t* fix = reinterpret_cast<uint16_t*>(out + m);  // kWin: buckets crossing a 32-column window edge
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t sitemask = (1u << sitebits) - 1;
   const int per = (nw + kCsThreads - 1) / kCsThreads;  // counter words owned by a thread in the scan
@@ -557,81 +556,30 @@ __global__ void __launch_bounds__(kCsThreads, 2)
       out[(old >> sh) & 0xffffu] = (c << sitebits) | (uint32_t)x;
     });
     __syncthreads();
-    OrdT* orow = ord + (size_t)r * Wp;
-    DistT* drow = dist + (size_t)r * Wp;
-    // bucket b = [end(b-1), end(b)): the cursors are now at the bucket ends
-    auto bucket_end = [&](int b) -> int { return b < 0 ? 0 : (int)((cnt[b >> 1] >> ((b & 1) << 4)) & 0xffffu); };
-    auto insertion_sort = [&](int s0, int e) {  // by site (same cost)
-      for (int i = s0 + 1; i < e; ++i) {
+    for (int b = tid; b < nb; b += kCsThreads) {  // bucket b = [end(b-1), end(b)), cursors now at the ends
+      const uint32_t e = (cnt[b >> 1] >> ((b & 1) << 4)) & 0xffffu;
+      const uint32_t s0 = b == 0 ? 0u : (cnt[(b - 1) >> 1] >> (((b - 1) & 1) << 4)) & 0xffffu;
+      for (uint32_t i = s0 + 1; i < e; ++i) {  // insertion sort by site (same cost)
         const uint32_t key = out[i];
-        int j = i;
+        uint32_t j = i;
         while (j > s0 && out[j - 1] > key) {
           out[j] = out[j - 1];
           --j;
         }
         out[j] = key;
       }
-    };
-    if constexpr (kWin) {
-      // Tie order by windows of 32 columns, one per warp step: a lane ranks
-      // its element among the same-cost elements of its window (shuffles,
-      // as many steps as the window's largest bucket) and writes it straight
-      // to the tables; a bucket crossing a window edge is listed and sorted
-      // by one thread afterwards.  Every lane does the same few steps, where
-      // a thread per bucket runs its bucket's quadratic insertion sort.
-      if (tid == 0) nfix = 0;
-      __syncthreads();
-      for (int base = warp * 32; base < m; base += kCsThreads) {
-        const int k = base + lane;
-        uint32_t key = 0;
-        int s0 = 0, e = 0;
-        if (k < m) {
-          key = out[k];
-          const int c = (int)(key >> sitebits);
-          s0 = bucket_end(c - 1);
-          e = bucket_end(c);
-          if (lane == 0 && s0 < base && s0 >= base - 32) fix[atomicAdd(&nfix, 1)] = (uint16_t)c;
-        }
-        const bool inwin = k < m && s0 >= base && e <= base + 32;
-        const int len = inwin ? e - s0 : 0;
-        const int steps = __reduce_max_sync(kFull, (unsigned)len);
-        int rank = 0;
-        for (int d = 0; d < steps; ++d) {
-          const uint32_t v = __shfl_sync(kFull, key, (s0 + d - base) & 31);
-          rank += (d < len && v < key) ? 1 : 0;
-        }
-        const int pos = s0 + rank;
-        if (inwin && pos < W) {
-          orow[pos] = (OrdT)(key & sitemask);
-          drow[pos] = (DistT)(key >> sitebits);
-        }
-      }
-      __syncthreads();
-      for (int x = tid; x < nfix; x += kCsThreads) {
-        const int c = fix[x], s0 = bucket_end(c - 1), e = bucket_end(c);
-        insertion_sort(s0, e);
-        for (int i = s0; i < min(e, W); ++i) {
-          const uint32_t key = out[i];
-          orow[i] = (OrdT)(key & sitemask);
-          drow[i] = (DistT)(key >> sitebits);
-        }
-      }
-      for (int k = W + tid; k < Wp; k += kCsThreads) {
+    }
+    __syncthreads();
+    OrdT* orow = ord + (size_t)r * Wp;
+    DistT* drow = dist + (size_t)r * Wp;
+    for (int k = tid; k < Wp; k += kCsThreads) {
+      if (k < W) {
+        const uint32_t key = out[k];
+        orow[k] = (OrdT)(key & sitemask);
+        drow[k] = (DistT)(key >> sitebits);
+      } else {
         orow[k] = (OrdT)m;  // sentinel: T[m] == 0, never open
         drow[k] = (DistT)0;
-      }
-    } else {
-      for (int b = tid; b < nb; b += kCsThreads) insertion_sort(bucket_end(b - 1), bucket_end(b));
-      __syncthreads();
-      for (int k = tid; k < Wp; k += kCsThreads) {
-        if (k < W) {
-          const uint32_t key = out[k];
-          orow[k] = (OrdT)(key & sitemask);
-          drow[k] = (DistT)(key >> sitebits);
-        } else {
-          orow[k] = (OrdT)m;  // sentinel: T[m] == 0, never open
-          drow[k] = (DistT)0;
-        }
       }
     }
     __syncthreads();
@@ -642,8 +590,7 @@ __global__ void __launch_bounds__(kCsThreads, 2)
 constexpr int kCsMaxM = 65535;
 
 size_t cs_smem(int m, int costbits) {
-  // counters, the row, and the window pass's list of edge-crossing buckets
-  return m > kCsMaxM ? ~(size_t)0 : ((size_t)1 << costbits) / 2 * 4 + (size_t)m * 4 + ((size_t)m / 32 + 2) * 2;
+  return m > kCsMaxM ? ~(size_t)0 : ((size_t)1 << costbits) / 2 * 4 + (size_t)m * 4;
 }
 
 // ---- site-major narrow cost matrix for the gather-min kernel (K2b) --------
@@ -696,17 +643,14 @@ static cudaError_t launch_rows_t(const BuildPlan& bp, const int64_t* costs, cons
       const size_t cs = cs_smem(bp.m, bp.cs_bits);
       cudaError_t e = cudaMemsetAsync(rows, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
-      // PMB_K1_WIN=0: the thread-per-bucket tie sort (A/B)
-      const char* ew = getenv("PMB_K1_WIN");
-      const bool win = !(ew && ew[0] == '0');
       if (c16) {
-        auto kern = win ? k_build_rows_cs<OrdT, DistT, uint16_t, true> : k_build_rows_cs<OrdT, DistT, uint16_t, false>;
+        auto kern = k_build_rows_cs<OrdT, DistT, uint16_t>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
         if (e != cudaSuccess) return e;
         kern<<<bp.cs_grid, kCsThreads, cs, st>>>(c16, bp.mP, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.cs_bits,
                                                   (OrdT*)ord, (DistT*)dist, rows);
       } else {
-        auto kern = win ? k_build_rows_cs<OrdT, DistT, int64_t, true> : k_build_rows_cs<OrdT, DistT, int64_t, false>;
+        auto kern = k_build_rows_cs<OrdT, DistT, int64_t>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
         if (e != cudaSuccess) return e;
         kern<<<bp.cs_grid, kCsThreads, cs, st>>>(costs, bp.m, bp.n, bp.m, bp.W, bp.Wp, bp.sitebits, bp.cs_bits,
