@@ -475,15 +475,15 @@ static int evaluate_host(pm_ctx* c, const uint64_t* bitsets, size_t count, size_
   // kernels of chunk k, so only the first chunk's copy is exposed.  Each extra
   // launch costs a CTA-segment tail (round 1: equal chunks only paid off from
   // 8192 chromosomes and 16 MB on), so a batch of >= 4 MB is split into a short
-  // lead chunk (an eighth: its copy is the exposed part) and the rest;
+  // lead chunk (a twelfth: its copy is the exposed part) and the rest;
   // PMB_H2D_LEAD=0 sends it in one piece, PMB_H2D_LEAD=<d> leads with 1/d.
   // Measured at syn20k, host-clock e2e (profiles/r02_e2e_ab.log): one piece
-  // 2.44 M evals/s, lead 1/8 2.47 M, 1/4 2.42 M, 1/2 2.35 M.
+  // 2.63 M evals/s, lead 1/6 2.75 M, 1/8 2.80 M, 1/12 2.82 M, 1/16 2.76 M.
   const size_t bytes = count * words_per * 8;
   std::vector<size_t> starts{0};
   {
     const char* le = getenv("PMB_H2D_LEAD");
-    const size_t lead_div = le ? (size_t)std::atoll(le) : 8;
+    const size_t lead_div = le ? (size_t)std::atoll(le) : 12;
     const int equal = (int)std::max<size_t>(
         1, std::min<size_t>({(size_t)kErrSlots - 1, count / 8192, bytes / (16u << 20)}));
     if (equal > 1) {
