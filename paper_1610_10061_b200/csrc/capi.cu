@@ -351,10 +351,11 @@ static bool scan_fits(pm_ctx* c, size_t count) {
 // (time ~ b p), so they meet near p* ~ sqrt(a m / b); the n=m=10000 sweep
 // (scan 1.177 / 0.701 ms, gather 0.479 / 0.805 ms at p = 50 / 100) puts it at
 // p* = 93, i.e. p* ~ 0.93 sqrt(m).
+static double auto_pstar(int m) { return 0.93 * std::sqrt((double)m); }
+
 static int auto_kind(pm_ctx* c, size_t count) {
   if (!scan_fits(c, count)) return PM_EVAL_GATHER;
-  const double pstar = 0.93 * std::sqrt((double)c->t.m);
-  return (double)c->t.p >= pstar ? PM_EVAL_SCAN : PM_EVAL_GATHER;
+  return (double)c->t.p >= auto_pstar(c->t.m) ? PM_EVAL_SCAN : PM_EVAL_GATHER;
 }
 
 int pm_auto_eval_kernel(pm_ctx* c) {
@@ -372,12 +373,22 @@ int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcos
   const DevTables& t = c->t;
   const int wp = (t.m + 63) / 64;
   unsigned long long* errw = errw_override ? errw_override : c->errw.as<unsigned long long>();
-  int kind = c->eval_kind == PM_EVAL_AUTO ? auto_kind(c, count) : c->eval_kind;
+  // one plan per evaluation (AUTO's fit check reuses it)
+  ScanPlan sp;
+  bool planned = false;
+  auto plan = [&]() {
+    if (!planned) sp = plan_scan(t, count, c->sms, c->max_smem, mode == 2);
+    planned = true;
+    return sp;
+  };
+  int kind = c->eval_kind;
   if (mode == 1) kind = PM_EVAL_GATHER;
-  if (mode == 2) kind = PM_EVAL_SCAN;
+  else if (mode == 2) kind = PM_EVAL_SCAN;
+  else if (kind == PM_EVAL_AUTO)
+    kind = (double)t.p >= auto_pstar(t.m) && plan().ctas > 0 ? PM_EVAL_SCAN : PM_EVAL_GATHER;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (kind == PM_EVAL_SCAN) {
-    const ScanPlan sp = plan_scan(t, count, c->sms, c->max_smem, mode == 2);
+    plan();
     if (sp.ctas == 0)
       return c->fail(PM_DOMAIN, "instance too large for the scan kernel's shared-memory masks; use PM_EVAL_GATHER");
     const size_t groups = (count + 63) / 64;

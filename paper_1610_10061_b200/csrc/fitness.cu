@@ -29,8 +29,11 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <cstring>
 #include <utility>
 #include <vector>
 
@@ -613,7 +616,37 @@ static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool t
   return acc32 ? scan_fn_acc<uint32_t, uint64_t, uint32_t>(G, ts) : scan_fn_acc<uint32_t, uint64_t, uint64_t>(G, ts);
 }
 
+// The planner's tuning overrides (PMB_SCAN_*; A/B experiments and tests), read
+// in one pass over the environment: plan_scan runs once per evaluation and
+// six getenv calls cost ~1 us of host time each time.
+struct ScanKnobs {
+  const char* shape = nullptr;      // "G,warps[,ctas per SM]": pins the shape
+  const char* wide = nullptr;       // "0": no many-warp variant
+  const char* pair = nullptr;       // "0"/"1": column pairs off/on
+  const char* coop = nullptr;       // clients per warp at which the cooperative tail starts
+  const char* coopseg = nullptr;    // log2 of the most lanes per client in the tail
+  const char* tailclaim = nullptr;  // clients left per warp below which claims shrink
+};
+
+static ScanKnobs scan_knobs() {
+  ScanKnobs k;
+  for (char** e = environ; e && *e; ++e) {
+    const char* v = *e;
+    if (std::strncmp(v, "PMB_SCAN_", 9) != 0) continue;
+    v += 9;
+    const struct { const char* name; const char** out; } names[] = {
+        {"SHAPE=", &k.shape}, {"WIDE=", &k.wide}, {"PAIR=", &k.pair},
+        {"COOP=", &k.coop}, {"COOPSEG=", &k.coopseg}, {"TAILCLAIM=", &k.tailclaim}};
+    for (const auto& nm : names) {
+      const size_t l = std::strlen(nm.name);
+      if (std::strncmp(v, nm.name, l) == 0) *nm.out = v + l;
+    }
+  }
+  return k;
+}
+
 ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, bool depth_mode) {
+  const ScanKnobs knob = scan_knobs();
   ScanPlan sp;
   // (group width, warps per CTA, CTAs per SM, masks in smem?) in preference
   // order.  Measured on B200 (profiles/r01_ncu_kernels.md):
@@ -639,7 +672,7 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
   const long long units_per_sm = ((long long)((count + 31) / 32) * t.n + sms - 1) / sms;
   const bool split = std::min<long long>(units_per_sm, t.n) < 4096;
   // PMB_SCAN_SHAPE="G,warps[,ctas per SM]" pins the shape (tuning experiments only)
-  const char* force = getenv("PMB_SCAN_SHAPE");
+  const char* force = knob.shape;
   int fG = 0, fW = 0, fC = 1;
   if (force) sscanf(force, "%d,%d,%d", &fG, &fW, &fC);
   for (const auto& sh0 : shapes) {
@@ -678,7 +711,7 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
         // mid-chunk when it could overflow) -- measured 7 % faster at syn20k
         // than 16 warps with three chunks (tools/wide_sweep.sh: 20-32 warps,
         // 64-256 records); PMB_SCAN_WIDE=0 turns it off
-        const char* ew = getenv("PMB_SCAN_WIDE");
+        const char* ew = knob.wide;
         if (!fG && !split && !(ew && ew[0] == '0') && sp.G == 32 && sp.tsmem && sp.acc32 && !depth_mode &&
             t.site_bytes == 2 && t.dist_bytes == 2) {
           const size_t sm2 = scan_smem(t.m, kWideWarps, true, true, 32, kWideQueue);
@@ -692,7 +725,7 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
             // columns.  syn20k 1.41 -> 1.40 ms, sweep p=50 1.42 -> 1.31 ms,
             // p=100 0.78 -> 0.76 ms; at p >= 200 the extra empty records of
             // the denser hits cost more (0.46 -> 0.48 ms) (profiles/r02_k2_ab.md)
-            const char* ep = getenv("PMB_SCAN_PAIR");
+            const char* ep = knob.pair;
             sp.pair = ep ? ep[0] == '1' : (long long)t.m >= 75LL * std::max(t.p, 1);
           }
         }
@@ -717,11 +750,11 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
         // cooperative tail (k_scan): a warp's last <= kCoop clients walk on
         // lane segments (profiles/r02_k2_ab.md; PMB_SCAN_COOP=<clients> and
         // PMB_SCAN_COOPSEG=<log2 most lanes per client> for A/B runs)
-        const char* ec = getenv("PMB_SCAN_COOP");
-        const char* es = getenv("PMB_SCAN_COOPSEG");
+        const char* ec = knob.coop;
+        const char* es = knob.coopseg;
         sp.coop = std::min(32, std::max(0, ec ? std::atoi(ec) : kCoop)) |
                   (std::min(5, std::max(0, es ? std::atoi(es) : 5)) << 8);
-        const char* et = getenv("PMB_SCAN_TAILCLAIM");  // clients left per warp (x warps)
+        const char* et = knob.tailclaim;  // clients left per warp (x warps)
         sp.tail_claim = (et ? std::atoi(et) : kTailClaim) * sp.warps;
         return sp;
       }
