@@ -78,7 +78,7 @@ void pm_destroy(pm_ctx* c) {
                     &c->ga.next, &c->ga.cost, &c->ga.before, &c->ga.child, &c->ga.ccost, &c->ga.ok,
                     &c->ga.brec, &c->ga.evals, &c->ga.tmp, &c->ga.table, &c->ga.ranks, &c->ga.rflags,
                     &c->ga.rstate, &c->ga.lfact, &c->ga.grec, &c->ga.gstate, &c->ga.perk, &c->sort_rows,
-                    &c->c16, &c->dT16})
+                    &c->c16, &c->dT16, &c->gsync})
     b->release();
   c->ga.hrec.release();
   c->ga.hglob.release();
@@ -402,6 +402,24 @@ int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcos
     }
     PM_CUDA_TRY(c, launch_scan(t, sp, c->T.as<uint64_t>(), count,
                                reinterpret_cast<unsigned long long*>(dcosts), errw, mode == 2, c->stream));
+  } else if (gather_fused_fits(t)) {
+    // one launch: lists in shared memory, costs stored; the error handoff
+    // words are armed once per context
+    if (!c->gsync.p) {
+      PM_CUDA_TRY(c, c->gsync.ensure(16));
+      PM_CUDA_TRY(c, cudaMemsetAsync(c->gsync.p, 0xff, 8, c->stream));
+      PM_CUDA_TRY(c, cudaMemsetAsync(c->gsync.as<char>() + 8, 0, 8, c->stream));
+    }
+    if (c->profiling) {
+      ev = c->ev_get();
+      cudaEventRecord(ev.first, c->stream);
+    }
+    PM_CUDA_TRY(c, launch_gather_fused(t, dwords, count, wp, reinterpret_cast<unsigned long long*>(dcosts),
+                                       c->gsync.as<unsigned long long>(),
+                                       reinterpret_cast<unsigned int*>(c->gsync.as<char>() + 8),
+                                       errw_override ? errw_override : errw, errw_override != nullptr, mode,
+                                       c->sms, c->stream));
+    c->launches -= 1;  // one launch, not two
   } else {
     PM_CUDA_TRY(c, c->lists.ensure(count * (size_t)c->open_cap * 4));
     PM_CUDA_TRY(c, c->counts.ensure(count * 4));

@@ -220,6 +220,188 @@ __global__ void __launch_bounds__(kGatherThreads, PMB_GATHER_MINB)
   }
 }
 
+// ---- K2b fused: one CTA per chromosome (n <= 1024 V clients) ----------------
+//
+// The same gather-min with the open-site list built by the CTA itself in shared
+// memory (a block scan over the chromosome's words) and the chromosome's cost
+// written with a plain store: no list kernel, no zeroed cost array, one launch.
+// Errors go to a context word that stays "none" between calls: CTAs atomicMin
+// into it, and the last CTA to finish (threadfence + arrival counter, the
+// counter reset by that CTA) hands the value to the call's error word -- a
+// store for a host call's per-chunk slot, a min into the sticky context word --
+// and re-arms it.
+template <class DistT, class OrdT>
+__global__ void __launch_bounds__(1024)
+    k_gather_fused(const DistT* __restrict__ dT, int nP, const OrdT* __restrict__ ord,
+                   const DistT* __restrict__ dist, int n, int m, int p, int W, int Wp,
+                   const uint64_t* __restrict__ words, int wp, size_t count,
+                   unsigned long long* __restrict__ costs, unsigned long long* err_work,
+                   unsigned int* done, unsigned long long* err_out, int err_store, int mode) {
+  using Vec = GVec<DistT>;
+  constexpr int V = Vec::V;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* list = reinterpret_cast<uint32_t*>(smem);  // the open sites, ascending
+  __shared__ unsigned long long red[32];
+  __shared__ uint32_t wtot[32];
+  __shared__ int anybad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int i0 = tid * V;
+  const int nv = i0 < n ? min(V, n - i0) : 0;
+  const DistT* col = dT + i0;
+  for (size_t c = blockIdx.x; c < count; c += gridDim.x) {
+    // 1. the open-site list: a block scan of the words' popcounts
+    const uint64_t* w = words + c * wp;
+    uint32_t total = 0;
+    if (tid == 0) anybad = 0;
+    for (int w0 = 0; w0 < wp; w0 += blockDim.x) {
+      const int wi = w0 + tid;
+      uint64_t x = wi < wp ? __ldg(w + wi) : 0;
+      if (wi == wp - 1 && (m & 63)) x &= (1ull << (m & 63)) - 1;  // bits >= m are not sites
+      const uint32_t pc = __popcll(x);
+      uint32_t incl = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wtot[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t v = lane < nwarps ? wtot[lane] : 0;
+        uint32_t wi2 = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(kFull, wi2, o);
+          if (lane >= o) wi2 += t;
+        }
+        if (lane < nwarps) wtot[lane] = wi2 - v;  // exclusive warp offsets
+        if (lane == 31) red[0] = wi2;           // this pass's total
+      }
+      __syncthreads();
+      uint32_t pos = total + wtot[warp] + incl - pc;
+      while (x) {
+        list[pos++] = (uint32_t)(wi * 64 + __ffsll((long long)x) - 1);
+        x &= x - 1;
+      }
+      total += (uint32_t)red[0];
+      __syncthreads();
+    }
+    // 2. the chromosome's cost over this thread's V clients
+    unsigned long long sum = 0;
+    bool bad = false;
+    if (total == 0) {
+      bad = true;  // no open site at all
+    } else if (!(mode == 0 && total < (uint32_t)p)) {
+      // common case: min over the list, V clients per 16-byte load, 8 in flight
+      Vec best;
+      best.set_max();
+      if (nv > 0) {
+        uint32_t t = 0;
+        for (; t + 8 <= total; t += 8) {
+          const uint4 ja = *reinterpret_cast<const uint4*>(list + t);
+          const uint4 jb = *reinterpret_cast<const uint4*>(list + t + 4);
+          const uint32_t js[8] = {ja.x, ja.y, ja.z, ja.w, jb.x, jb.y, jb.z, jb.w};
+          uint4 xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) xv[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)js[u] * nP));
+#pragma unroll
+          for (int u = 0; u < 8; ++u) best.min_with(xv[u]);
+        }
+        for (; t < total; ++t) best.min_with(__ldg(reinterpret_cast<const uint4*>(col + (size_t)list[t] * nP)));
+#pragma unroll
+        for (int q = 0; q < V; ++q)
+          if (q < nv) sum += best.elem(q);
+      }
+    } else {
+      // fewer than p open sites under the fitness contract: the (cost, site)
+      // smallest open site (ascending list, strict <: the lowest site on ties)
+      // must not sort after column W-1 (ordering.cpp:50-52)
+      for (int q = 0; q < nv; ++q) {
+        const int i = i0 + q;
+        uint64_t bv = ~0ull;
+        uint32_t bj = 0;
+        for (uint32_t t = 0; t < total; ++t) {
+          const uint32_t j = list[t];
+          const uint64_t v = (uint64_t)dT[(size_t)j * nP + i];
+          if (v < bv) {
+            bv = v;
+            bj = j;
+          }
+        }
+        sum += bv;
+        const uint64_t dlast = (uint64_t)dist[(size_t)i * Wp + (W - 1)];
+        const uint32_t jlast = (uint32_t)ord[(size_t)i * Wp + (W - 1)];
+        bad |= !(bv < dlast || (bv == dlast && bj <= jlast));
+      }
+    }
+    // 3. block sum; the cost is written, the failure reported once
+    sum = warp_sum(sum);
+    if (__any_sync(kFull, bad) && lane == 0) anybad = 1;
+    if (lane == 0) red[warp] = sum;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long s = 0;
+      for (int x = 0; x < nwarps; ++x) s += red[x];
+      costs[c] = s;
+      if (anybad) atomicMin(err_work, (unsigned long long)c);
+    }
+    __syncthreads();  // list, red and anybad are rewritten for the next chromosome
+  }
+  // 4. the last CTA hands the error word over and re-arms it
+  if (tid == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(done, 1u);
+    if (t == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long v = atomicExch(err_work, ~0ull);
+      *done = 0;
+      if (err_store) *err_out = v;
+      else if (v != ~0ull) atomicMin(err_out, v);
+    }
+  }
+}
+
+template <class DistT, class OrdT>
+static cudaError_t launch_gather_fused_t(const DevTables& t, const uint64_t* words, size_t count, int wp,
+                                         unsigned long long* costs, unsigned long long* err_work,
+                                         unsigned int* done, unsigned long long* err_out, int err_store,
+                                         int mode, int sms, cudaStream_t st) {
+  constexpr int V = 16 / sizeof(DistT);
+  const int threads = ((t.n + V - 1) / V + 31) / 32 * 32;
+  const size_t smem = ((size_t)t.m + 8) * 4;
+  auto kern = k_gather_fused<DistT, OrdT>;
+  static thread_local size_t raised = 0;
+  if (smem > 48 * 1024 && smem > raised) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    raised = smem;
+  }
+  const int per_sm = std::max(1, std::min(2048 / threads, (int)((200u << 10) / (smem + 1024))));
+  const unsigned grid = (unsigned)std::min<size_t>(count, (size_t)sms * per_sm * 4);
+  kern<<<grid, threads, smem, st>>>((const DistT*)t.dT, t.nP, (const OrdT*)t.ord, (const DistT*)t.dist, t.n, t.m,
+                                    t.p, t.W, t.Wp, words, wp, count, costs, err_work, done, err_out, err_store,
+                                    mode);
+  return cudaGetLastError();
+}
+
+bool gather_fused_fits(const DevTables& t) {
+  const int V = 16 / t.dist_bytes;
+  return (t.n + V - 1) / V <= 1024 && t.m <= 16384;
+}
+
+cudaError_t launch_gather_fused(const DevTables& t, const uint64_t* words, size_t count, int words_per,
+                                unsigned long long* costs, unsigned long long* err_work, unsigned int* done,
+                                unsigned long long* err_out, int err_store, int mode, int sms, cudaStream_t st) {
+  if (t.site_bytes == 2) {
+    if (t.dist_bytes == 2) return launch_gather_fused_t<uint16_t, uint16_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
+    if (t.dist_bytes == 4) return launch_gather_fused_t<uint32_t, uint16_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
+    return launch_gather_fused_t<uint64_t, uint16_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
+  }
+  if (t.dist_bytes == 2) return launch_gather_fused_t<uint16_t, uint32_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
+  if (t.dist_bytes == 4) return launch_gather_fused_t<uint32_t, uint32_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
+  return launch_gather_fused_t<uint64_t, uint32_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
+}
+
 template <class DistT, class OrdT>
 static cudaError_t launch_gather_t(const DevTables& t, const uint64_t* words, size_t count, int wp,
                                    const uint32_t* lists, const uint32_t* counts, int cap,
