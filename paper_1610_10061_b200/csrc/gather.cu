@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kGatherThreads, PMB_GATHER_MINB)
 // store for a host call's per-chunk slot, a min into the sticky context word --
 // and re-arms it.
 template <class DistT, class OrdT>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(1024, 2)  // <= 32 registers: three 640-thread CTAs per SM at syn5k
     k_gather_fused(const DistT* __restrict__ dT, int nP, const OrdT* __restrict__ ord,
                    const DistT* __restrict__ dist, int n, int m, int p, int W, int Wp,
                    const uint64_t* __restrict__ words, int wp, size_t count,
