@@ -78,7 +78,7 @@ void pm_destroy(pm_ctx* c) {
                     &c->ga.next, &c->ga.cost, &c->ga.before, &c->ga.child, &c->ga.ccost, &c->ga.ok,
                     &c->ga.brec, &c->ga.evals, &c->ga.tmp, &c->ga.table, &c->ga.ranks, &c->ga.rflags,
                     &c->ga.rstate, &c->ga.lfact, &c->ga.grec, &c->ga.gstate, &c->ga.perk, &c->sort_rows,
-                    &c->c16, &c->dT16, &c->gsync})
+                    &c->c16, &c->dT16, &c->gsync, &c->gpart, &c->garr})
     b->release();
   c->ga.hrec.release();
   c->ga.hglob.release();
@@ -414,7 +414,18 @@ int evaluate_core(pm_ctx* c, const uint64_t* dwords, size_t count, int64_t* dcos
       ev = c->ev_get();
       cudaEventRecord(ev.first, c->stream);
     }
+    // several client slabs per chromosome: partial sums + arrival counters
+    // (grown zeroed; the kernel leaves them at 0)
+    const int ns = gather_fused_slabs(t);
+    if (ns > 1) {
+      PM_CUDA_TRY(c, c->gpart.ensure(count * ns * 8));
+      if (c->garr.bytes < count * 4) {
+        PM_CUDA_TRY(c, c->garr.ensure(count * 4));
+        PM_CUDA_TRY(c, cudaMemsetAsync(c->garr.p, 0, c->garr.bytes, c->stream));
+      }
+    }
     PM_CUDA_TRY(c, launch_gather_fused(t, dwords, count, wp, reinterpret_cast<unsigned long long*>(dcosts),
+                                       c->gpart.as<unsigned long long>(), c->garr.as<unsigned int>(),
                                        c->gsync.as<unsigned long long>(),
                                        reinterpret_cast<unsigned int*>(c->gsync.as<char>() + 8),
                                        errw_override ? errw_override : errw, errw_override != nullptr, mode,

@@ -109,6 +109,7 @@ struct pm_ctx {
   DevBuf costs_in, sort_keys, sort_pay, sort_rows, words, costs_out, T, lists, counts, errw, scal;
   DevBuf c16, dT16;  // set_instance scratch: the u16 cost copies of the fused prep pass
   DevBuf gsync;      // fused gather: error word (kept at ~0) + arrival counter (kept at 0)
+  DevBuf gpart, garr;  // fused gather over client slabs: partial sums, per-chromosome counters (kept at 0)
   pmb::HostBuf hout;  // host-buffer calls: costs + error words come back in one pinned copy
   int open_cap = 0;
   GaBuffers ga;

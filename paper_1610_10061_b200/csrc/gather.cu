@@ -220,35 +220,41 @@ __global__ void __launch_bounds__(kGatherThreads, PMB_GATHER_MINB)
   }
 }
 
-// ---- K2b fused: one CTA per chromosome (n <= 1024 V clients) ----------------
+// ---- K2b fused: lists in shared memory, one launch ---------------------------
 //
-// The same gather-min with the open-site list built by the CTA itself in shared
-// memory (a block scan over the chromosome's words) and the chromosome's cost
-// written with a plain store: no list kernel, no zeroed cost array, one launch.
-// Errors go to a context word that stays "none" between calls: CTAs atomicMin
-// into it, and the last CTA to finish (threadfence + arrival counter, the
-// counter reset by that CTA) hands the value to the call's error word -- a
-// store for a host call's per-chunk slot, a min into the sticky context word --
-// and re-arms it.
+// The same gather-min with the open-site list built by each CTA in shared
+// memory (a block scan over the chromosome's words; u16 entries) and no zeroed
+// cost array: a work item is (chromosome, slab of <= 1024 x V clients).  With
+// one slab the CTA stores the chromosome's cost; with several, each stores its
+// partial sum and the last slab to arrive (threadfence + a per-chromosome
+// counter it resets) adds them and stores the cost.  Errors go to a context
+// word that stays "none" between calls: CTAs atomicMin into it, and the last
+// CTA to finish (threadfence + arrival counter, reset by that CTA) hands the
+// value to the call's error word -- a store for a host call's per-chunk slot, a
+// min into the sticky context word -- and re-arms it.
 template <class DistT, class OrdT>
 __global__ void __launch_bounds__(1024, 2)  // <= 32 registers: three 640-thread CTAs per SM at syn5k
     k_gather_fused(const DistT* __restrict__ dT, int nP, const OrdT* __restrict__ ord,
                    const DistT* __restrict__ dist, int n, int m, int p, int W, int Wp,
-                   const uint64_t* __restrict__ words, int wp, size_t count,
-                   unsigned long long* __restrict__ costs, unsigned long long* err_work,
-                   unsigned int* done, unsigned long long* err_out, int err_store, int mode) {
+                   const uint64_t* __restrict__ words, int wp, size_t count, int nslab,
+                   unsigned long long* __restrict__ costs, unsigned long long* partial, unsigned int* arrive,
+                   unsigned long long* err_work, unsigned int* done, unsigned long long* err_out, int err_store,
+                   int mode) {
   using Vec = GVec<DistT>;
   constexpr int V = Vec::V;
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* list = reinterpret_cast<uint32_t*>(smem);  // the open sites, ascending
+  uint16_t* list = reinterpret_cast<uint16_t*>(smem);  // the open sites, ascending (m <= 65535)
   __shared__ unsigned long long red[32];
   __shared__ uint32_t wtot[32];
-  __shared__ int anybad;
+  __shared__ int anybad, last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int i0 = tid * V;
-  const int nv = i0 < n ? min(V, n - i0) : 0;
-  const DistT* col = dT + i0;
-  for (size_t c = blockIdx.x; c < count; c += gridDim.x) {
+  const size_t items = count * (size_t)nslab;
+  for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const size_t c = it / nslab;
+    const int slab = (int)(it % nslab);
+    const int i0 = (slab * (int)blockDim.x + tid) * V;  // first client of this thread
+    const int nv = i0 < n ? min(V, n - i0) : 0;
+    const DistT* col = dT + i0;
     // 1. the open-site list: a block scan of the words' popcounts
     const uint64_t* w = words + c * wp;
     uint32_t total = 0;
@@ -280,13 +286,13 @@ __global__ void __launch_bounds__(1024, 2)  // <= 32 registers: three 640-thread
       __syncthreads();
       uint32_t pos = total + wtot[warp] + incl - pc;
       while (x) {
-        list[pos++] = (uint32_t)(wi * 64 + __ffsll((long long)x) - 1);
+        list[pos++] = (uint16_t)(wi * 64 + __ffsll((long long)x) - 1);
         x &= x - 1;
       }
       total += (uint32_t)red[0];
       __syncthreads();
     }
-    // 2. the chromosome's cost over this thread's V clients
+    // 2. this slab's share of the chromosome's cost
     unsigned long long sum = 0;
     bool bad = false;
     if (total == 0) {
@@ -298,9 +304,9 @@ __global__ void __launch_bounds__(1024, 2)  // <= 32 registers: three 640-thread
       if (nv > 0) {
         uint32_t t = 0;
         for (; t + 8 <= total; t += 8) {
-          const uint4 ja = *reinterpret_cast<const uint4*>(list + t);
-          const uint4 jb = *reinterpret_cast<const uint4*>(list + t + 4);
-          const uint32_t js[8] = {ja.x, ja.y, ja.z, ja.w, jb.x, jb.y, jb.z, jb.w};
+          const uint4 jv = *reinterpret_cast<const uint4*>(list + t);  // 8 u16 site indices
+          const uint32_t js[8] = {jv.x & 0xffffu, jv.x >> 16, jv.y & 0xffffu, jv.y >> 16,
+                                  jv.z & 0xffffu, jv.z >> 16, jv.w & 0xffffu, jv.w >> 16};
           uint4 xv[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) xv[u] = __ldg(reinterpret_cast<const uint4*>(col + (size_t)js[u] * nP));
@@ -334,7 +340,8 @@ __global__ void __launch_bounds__(1024, 2)  // <= 32 registers: three 640-thread
         bad |= !(bv < dlast || (bv == dlast && bj <= jlast));
       }
     }
-    // 3. block sum; the cost is written, the failure reported once
+    // 3. block sum; the cost (or this slab's part of it) is stored, a failure
+    // reported by whichever slab sees it
     sum = warp_sum(sum);
     if (__any_sync(kFull, bad) && lane == 0) anybad = 1;
     if (lane == 0) red[warp] = sum;
@@ -342,10 +349,23 @@ __global__ void __launch_bounds__(1024, 2)  // <= 32 registers: three 640-thread
     if (tid == 0) {
       unsigned long long s = 0;
       for (int x = 0; x < nwarps; ++x) s += red[x];
-      costs[c] = s;
       if (anybad) atomicMin(err_work, (unsigned long long)c);
+      if (nslab == 1) {
+        costs[c] = s;
+      } else {
+        partial[it] = s;
+        __threadfence();
+        last = atomicAdd(arrive + c, 1u) == (unsigned)nslab - 1;
+        if (last) {
+          __threadfence();
+          unsigned long long tot = 0;
+          for (int k = 0; k < nslab; ++k) tot += *(volatile unsigned long long*)(partial + c * nslab + k);
+          costs[c] = tot;
+          arrive[c] = 0;  // re-armed for the next call
+        }
+      }
     }
-    __syncthreads();  // list, red and anybad are rewritten for the next chromosome
+    __syncthreads();  // list, red and the flags are rewritten for the next item
   }
   // 4. the last CTA hands the error word over and re-arms it
   if (tid == 0) {
@@ -361,14 +381,30 @@ __global__ void __launch_bounds__(1024, 2)  // <= 32 registers: three 640-thread
   }
 }
 
+// Work split: threads per CTA and client slabs per chromosome (balanced slabs
+// of at most 1024 threads).
+static void fused_split(const DevTables& t, int* threads, int* nslab) {
+  const int V = 16 / t.dist_bytes;
+  const int tn = (t.n + V - 1) / V;
+  *nslab = (tn + 1023) / 1024;
+  *threads = ((tn + *nslab - 1) / *nslab + 31) / 32 * 32;
+}
+
+int gather_fused_slabs(const DevTables& t) {
+  int th, ns;
+  fused_split(t, &th, &ns);
+  return ns;
+}
+
 template <class DistT, class OrdT>
 static cudaError_t launch_gather_fused_t(const DevTables& t, const uint64_t* words, size_t count, int wp,
-                                         unsigned long long* costs, unsigned long long* err_work,
-                                         unsigned int* done, unsigned long long* err_out, int err_store,
-                                         int mode, int sms, cudaStream_t st) {
-  constexpr int V = 16 / sizeof(DistT);
-  const int threads = ((t.n + V - 1) / V + 31) / 32 * 32;
-  const size_t smem = ((size_t)t.m + 8) * 4;
+                                         unsigned long long* costs, unsigned long long* partial,
+                                         unsigned int* arrive, unsigned long long* err_work, unsigned int* done,
+                                         unsigned long long* err_out, int err_store, int mode, int sms,
+                                         cudaStream_t st) {
+  int threads, nslab;
+  fused_split(t, &threads, &nslab);
+  const size_t smem = ((size_t)t.m + 16) * 2;
   auto kern = k_gather_fused<DistT, OrdT>;
   static thread_local size_t raised = 0;
   if (smem > 48 * 1024 && smem > raised) {
@@ -377,29 +413,31 @@ static cudaError_t launch_gather_fused_t(const DevTables& t, const uint64_t* wor
     raised = smem;
   }
   const int per_sm = std::max(1, std::min(2048 / threads, (int)((200u << 10) / (smem + 1024))));
-  const unsigned grid = (unsigned)std::min<size_t>(count, (size_t)sms * per_sm * 4);
+  const unsigned grid = (unsigned)std::min<size_t>(count * nslab, (size_t)sms * per_sm * 4);
   kern<<<grid, threads, smem, st>>>((const DistT*)t.dT, t.nP, (const OrdT*)t.ord, (const DistT*)t.dist, t.n, t.m,
-                                    t.p, t.W, t.Wp, words, wp, count, costs, err_work, done, err_out, err_store,
-                                    mode);
+                                    t.p, t.W, t.Wp, words, wp, count, nslab, costs, partial, arrive, err_work,
+                                    done, err_out, err_store, mode);
   return cudaGetLastError();
 }
 
-bool gather_fused_fits(const DevTables& t) {
-  const int V = 16 / t.dist_bytes;
-  return (t.n + V - 1) / V <= 1024 && t.m <= 16384;
-}
+bool gather_fused_fits(const DevTables& t) { return t.m <= 65535; }
 
 cudaError_t launch_gather_fused(const DevTables& t, const uint64_t* words, size_t count, int words_per,
-                                unsigned long long* costs, unsigned long long* err_work, unsigned int* done,
-                                unsigned long long* err_out, int err_store, int mode, int sms, cudaStream_t st) {
+                                unsigned long long* costs, unsigned long long* partial, unsigned int* arrive,
+                                unsigned long long* err_work, unsigned int* done, unsigned long long* err_out,
+                                int err_store, int mode, int sms, cudaStream_t st) {
+#define PMB_FUSED(D, O) \
+  return launch_gather_fused_t<D, O>(t, words, count, words_per, costs, partial, arrive, err_work, done, err_out, \
+                                     err_store, mode, sms, st)
   if (t.site_bytes == 2) {
-    if (t.dist_bytes == 2) return launch_gather_fused_t<uint16_t, uint16_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
-    if (t.dist_bytes == 4) return launch_gather_fused_t<uint32_t, uint16_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
-    return launch_gather_fused_t<uint64_t, uint16_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
+    if (t.dist_bytes == 2) PMB_FUSED(uint16_t, uint16_t);
+    if (t.dist_bytes == 4) PMB_FUSED(uint32_t, uint16_t);
+    PMB_FUSED(uint64_t, uint16_t);
   }
-  if (t.dist_bytes == 2) return launch_gather_fused_t<uint16_t, uint32_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
-  if (t.dist_bytes == 4) return launch_gather_fused_t<uint32_t, uint32_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
-  return launch_gather_fused_t<uint64_t, uint32_t>(t, words, count, words_per, costs, err_work, done, err_out, err_store, mode, sms, st);
+  if (t.dist_bytes == 2) PMB_FUSED(uint16_t, uint32_t);
+  if (t.dist_bytes == 4) PMB_FUSED(uint32_t, uint32_t);
+  PMB_FUSED(uint64_t, uint32_t);
+#undef PMB_FUSED
 }
 
 template <class DistT, class OrdT>

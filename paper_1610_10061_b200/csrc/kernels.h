@@ -94,15 +94,19 @@ cudaError_t launch_walks(const DevTables& t, const uint64_t* T, size_t count, un
 cudaError_t launch_open_lists(const uint64_t* words, size_t count, int words_per, int m,
                               uint32_t* open_lists, uint32_t* open_counts, int open_cap,
                               unsigned long long* costs, unsigned long long* err_init, cudaStream_t st);
-// K2b fused (n <= 1024 * 16/dist_bytes clients, m <= 16384): one launch per
-// evaluation, lists built in shared memory, costs stored (no zeroing needed).
-// err_work / done: a context word kept at ~0 and an arrival counter kept at 0
-// between calls; the last CTA writes the call's error into err_out (err_store:
-// a store, else a min into a sticky word) and re-arms them.
+// K2b fused (m <= 65535): one launch per evaluation, lists built in shared
+// memory, costs stored (no zeroing needed).  Work items are (chromosome, client
+// slab); with several slabs (gather_fused_slabs > 1) `partial` holds count x
+// slabs sums and `arrive` count counters kept at 0 between calls.  err_work /
+// done: a context word kept at ~0 and an arrival counter kept at 0 between
+// calls; the last CTA writes the call's error into err_out (err_store: a store,
+// else a min into a sticky word) and re-arms them.
 bool gather_fused_fits(const DevTables& t);
+int gather_fused_slabs(const DevTables& t);
 cudaError_t launch_gather_fused(const DevTables& t, const uint64_t* words, size_t count, int words_per,
-                                unsigned long long* costs, unsigned long long* err_work, unsigned int* done,
-                                unsigned long long* err_out, int err_store, int mode, int sms, cudaStream_t st);
+                                unsigned long long* costs, unsigned long long* partial, unsigned int* arrive,
+                                unsigned long long* err_work, unsigned int* done, unsigned long long* err_out,
+                                int err_store, int mode, int sms, cudaStream_t st);
 // K2b: gather-min (needs launch_open_lists first).  mode 0 = fitness semantics (scan-width contract), 1 = min_cost_sum.
 cudaError_t launch_gather(const DevTables& t, const uint64_t* words, size_t count, int words_per,
                           uint32_t* open_lists, uint32_t* open_counts, int open_cap,

@@ -22,9 +22,10 @@ def _gather(ctx, pm, words):
         ctx.set_eval_kernel(pm.EVAL_AUTO)
 
 
-@pytest.fixture
-def inst(ctx, oracle):
-    n, p = 3000, 30
+@pytest.fixture(params=[3000, 9500], ids=["one-slab", "two-slabs"])
+def inst(ctx, oracle, request):
+    n = request.param
+    p = n // 100
     costs = oracle.synth_euclid(n, seed=77)
     ctx.set_instance(costs, n, n, p)
     so, inc = oracle.build_ordering(n, n, p, costs)
