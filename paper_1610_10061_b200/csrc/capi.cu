@@ -348,10 +348,10 @@ static bool scan_fits(pm_ctx* c, size_t count) {
 
 // Measured crossover (profiles/r02_p_sweep.md): the scan touches
 // ~(m+1)/(p+1) columns per client (time ~ a m / p + c), the gather p sites
-// (time ~ b p), so they meet near p* ~ sqrt(a m / b); the n=m=10000 sweep
-// (scan 1.177 / 0.701 ms, gather 0.479 / 0.805 ms at p = 50 / 100) puts it at
-// p* = 93, i.e. p* ~ 0.93 sqrt(m).
-static double auto_pstar(int m) { return 0.93 * std::sqrt((double)m); }
+// (time ~ b p), so they meet near p* ~ sqrt(a m / b); the n=m=10000 sweep with
+// the fused gather (scan 0.700 / 0.408 ms, gather 0.621 / 0.943 ms at p = 100 /
+// 200) puts it at p* ~ 110, i.e. p* ~ 1.1 sqrt(m).
+static double auto_pstar(int m) { return 1.1 * std::sqrt((double)m); }
 
 static int auto_kind(pm_ctx* c, size_t count) {
   if (!scan_fits(c, count)) return PM_EVAL_GATHER;

@@ -22,7 +22,7 @@
 // owns 16 bytes of consecutive clients (8 at u16 costs); each open site j of a
 // chromosome is one 16-byte read of the site-major row dT[j][i0..] and a packed
 // min.  Wins when p is small (the scan reads ~m/p columns per client, the
-// gather p): AUTO picks the scan iff p >= 0.93 sqrt(m), measured.  The reference's scan-width contract
+// gather p): AUTO picks the scan iff p >= 1.1 sqrt(m), measured.  The reference's scan-width contract
 // (ordering.cpp:50-52) is enforced exactly: with popcount >= p it cannot fail
 // (W = m-p+1 columns always contain one of p distinct sites); with fewer open
 // sites the (cost, site)-smallest open site must not sort after column W-1.
