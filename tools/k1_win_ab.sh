@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical: the window tie pass was measured slower and removed -- DESIGN.md §4 K1; PMB_K1_WIN no longer exists)
 # K1 counting sort: window tie pass (default) vs the thread-per-bucket sort (PMB_K1_WIN=0):
 # table parity, set_instance wall times, and the kernel's ncu duration at syn20k.
 mkdir -p gpurun_out
