@@ -626,6 +626,7 @@ struct ScanKnobs {
   const char* coop = nullptr;       // clients per warp at which the cooperative tail starts
   const char* coopseg = nullptr;    // log2 of the most lanes per client in the tail
   const char* tailclaim = nullptr;  // clients left per warp below which claims shrink
+  const char* split = nullptr;      // clients per CTA segment below which the split shapes are used
 };
 
 static ScanKnobs scan_knobs() {
@@ -636,7 +637,7 @@ static ScanKnobs scan_knobs() {
     v += 9;
     const struct { const char* name; const char** out; } names[] = {
         {"SHAPE=", &k.shape}, {"WIDE=", &k.wide}, {"PAIR=", &k.pair},
-        {"COOP=", &k.coop}, {"COOPSEG=", &k.coopseg}, {"TAILCLAIM=", &k.tailclaim}};
+        {"COOP=", &k.coop}, {"COOPSEG=", &k.coopseg}, {"TAILCLAIM=", &k.tailclaim}, {"SPLIT=", &k.split}};
     for (const auto& nm : names) {
       const size_t l = std::strlen(nm.name);
       if (std::strncmp(v, nm.name, l) == 0) *nm.out = v + l;
@@ -658,8 +659,7 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
   //   n (pmed40) or few units per CTA (syn5k) -- the per-segment barriers leave
   //   warps idle, so the same 16 warps per SM run as 8 x 2 or 4 x 4 CTAs whose
   //   barriers overlap (pmed40 0.114 -> 0.082 ms, syn5k 0.181 -> 0.161 ms);
-  //   with long segments (>= 4096 clients) splitting is neutral, so one CTA
-  //   per SM is kept there.
+  //   with long segments (>= ~1350 clients per SM) the 24-warp CTA is faster.
   // The last entry reads the masks from global memory and always fits.
   const struct { int G, warps, cps; bool tsmem; } shapes[] = {
       {32, 2, 8, true}, {32, 4, 4, true}, {32, 8, 2, true},
@@ -670,7 +670,11 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
   const unsigned long long vmax = depth_mode ? (unsigned long long)t.Wp : (unsigned long long)t.max_cost;
   // clients per CTA segment (a segment never crosses a group)
   const long long units_per_sm = ((long long)((count + 31) / 32) * t.n + sms - 1) / sms;
-  const bool split = std::min<long long>(units_per_sm, t.n) < 4096;
+  // segments below ~1350 clients per SM (syn5k, the pmed40 shape, 256-chromosome
+  // syn20k batches) run the split shapes; above it the 24-warp CTA wins
+  // (syn20k 384-768 chromosomes: -4-6 %, profiles/r02_k2_ab.md)
+  const long long split_below = knob.split ? std::atoll(knob.split) : 1350;
+  const bool split = std::min<long long>(units_per_sm, t.n) < split_below;
   // PMB_SCAN_SHAPE="G,warps[,ctas per SM]" pins the shape (tuning experiments only)
   const char* force = knob.shape;
   int fG = 0, fW = 0, fC = 1;
