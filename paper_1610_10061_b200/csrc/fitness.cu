@@ -129,6 +129,10 @@ constexpr int kChunk = 16;  // columns per lane step (32 B of u16 sites)
 #define PMB_X_SHORT 1
 #endif
 constexpr int kWideWarps = 24, kWideQueue = 256;  // the many-warp K2 variant (plan_scan)
+#ifndef PMB_PAIRQ
+#define PMB_PAIRQ 192
+#endif
+constexpr int kPairQueue = PMB_PAIRQ;  // its column-pair CTA: 192 records (syn20k -1.2 % vs 256)
 constexpr int kCoop = 16;          // clients per warp at which the cooperative tail starts
 constexpr int kTailClaim = 32;     // clients left per warp below which claims shrink (tools/env_ab.sh)
 #ifndef PMB_QCHECK
@@ -136,6 +140,7 @@ constexpr int kTailClaim = 32;     // clients left per warp below which claims s
 #endif
 constexpr int kQCheck = PMB_QCHECK;  // columns between queue-overflow checks (many-warp variant)
 static_assert(16 % kQCheck == 0 && kWideQueue > 32 * kQCheck, "queue check stride");
+static_assert(kPairQueue % 2 == 0 && kPairQueue >= 64 && kPairQueue <= kWideQueue, "pair queue: whole pairs");
 
 template <class OrdT, class DistT>
 struct Chunk {
@@ -601,7 +606,7 @@ static const void* scan_kernel_ptr(const DevTables& t, bool acc32, int G, bool t
   if (wide && t.site_bytes == 2 && t.dist_bytes == 2 && acc32 && G == 32 && ts && !g_depth) {
     // wide = warps per CTA of the variant (kWideWarps: one CTA per SM)
     if (pair && wide == kWideWarps)
-      return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue, kWideWarps, true>);
+      return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kPairQueue, kWideWarps, true>);
     if (wide == 2) return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue, 2>);
     if (wide == 4) return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue, 4>);
     return reinterpret_cast<const void*>(k_scan<uint16_t, uint16_t, uint32_t, uint32_t, true, false, kWideWarps, kWideQueue>);
@@ -731,6 +736,7 @@ ScanPlan plan_scan(const DevTables& t, size_t count, int sms, size_t max_smem, b
             // the denser hits cost more (0.46 -> 0.48 ms) (profiles/r02_k2_ab.md)
             const char* ep = knob.pair;
             sp.pair = ep ? ep[0] == '1' : (long long)t.m >= 75LL * std::max(t.p, 1);
+            if (sp.pair) sp.smem = scan_smem(t.m, kWideWarps, true, true, 32, kPairQueue);
           }
         }
         // split shapes (short segments): the same variant as 12 x 2-warp (or
